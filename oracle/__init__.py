@@ -1,0 +1,7 @@
+"""float64 CPU oracle (TEST INFRASTRUCTURE ONLY).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+reference legs may import this package.  The product path
+(paper_2003_12693_b200) never imports it and shares no code with it.
+"""
+from .oracle import *  # noqa: F401,F403

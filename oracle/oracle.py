@@ -1,0 +1,249 @@
+"""ctypes wrapper around oracle/sr_oracle.c (plain C, float64).
+
+TEST INFRASTRUCTURE ONLY -- see oracle/__init__.py.  Every function converts
+its inputs to C-contiguous float64 and calls the C routine of the same name;
+there is no arithmetic of the method in this file.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "sr_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+__all__ = ["build", "Params", "H", "delta", "delta_prime", "h", "h_prime", "grad", "div", "edge",
+           "fft", "fft2", "symbol", "solve", "window_sum", "rhs", "shrink", "project", "wb",
+           "init", "sweep", "iterate", "label", "run", "lib"]
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (-O2 -ffp-contract=off -fopenmp, no fast-math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        cmd = ["gcc", "-std=c11", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC",
+               "-shared", "-o", _LIB, _SRC, "-lm"]
+        subprocess.check_call(cmd)
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(build())
+        d, i, p = C.c_double, C.c_int, C.c_void_p
+        sig = {
+            "orc_H": (d, [d, d]), "orc_delta": (d, [d, d]), "orc_delta_prime": (d, [d, d]),
+            "orc_h": (d, [d, d, d]), "orc_h_prime": (d, [d, d, d]),
+            "orc_grad": (None, [i, i, p, p, p]), "orc_div": (None, [i, i, p, p, p]),
+            "orc_edge": (None, [i, i, p, d, d, i, p]),
+            "orc_fft": (i, [i, p, p, i]), "orc_fft2": (i, [i, i, p, p, i]),
+            "orc_symbol": (d, [i, i, d, d, i, i]), "orc_solve": (i, [i, i, d, d, p, p]),
+            "orc_window_sum": (None, [i, i, i, d, i, p, p, p, p]),
+            "orc_rhs": (None, [i, i, p, p, p, p, p, p, p, p]),
+            "orc_shrink": (None, [d, d, d, p, p]), "orc_project": (None, [i, d, d, p, p]),
+            "orc_wb": (None, [i, i, p, p, p, p, p, p, p]),
+            "orc_init": (None, [i, i, p, p, p, p, p, p]),
+            "orc_sweep": (i, [i, i, p, p, p, p, p, p, p]),
+            "orc_iterate": (i, [i, i, p, p, p, p, p, p, p, i]),
+            "orc_label": (i, [i, i, p, i, p]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(_lib, name)
+            fn.restype = res
+            fn.argtypes = args
+    return _lib
+
+
+class Params(C.Structure):
+    """Mirror of orc_params in sr_oracle.c."""
+    _fields_ = [("gamma", C.c_double), ("alpha", C.c_double), ("beta", C.c_double), ("mu", C.c_double),
+                ("epsilon", C.c_double), ("l", C.c_double), ("d", C.c_double), ("window", C.c_int),
+                ("window_shape", C.c_int), ("tau", C.c_double), ("S", C.c_int), ("phi_clip", C.c_double),
+                ("w_proj", C.c_int), ("w_mode", C.c_int), ("w_iters", C.c_int)]
+
+    @classmethod
+    def from_dict(cls, p: dict) -> "Params":
+        q = cls()
+        for name, _ in cls._fields_:
+            setattr(q, name, p[name])
+        return q
+
+
+def _d(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _ptr(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _P(p):
+    return C.byref(p if isinstance(p, Params) else Params.from_dict(p))
+
+
+# pointwise ------------------------------------------------------------
+def H(x, eps):
+    return float(lib().orc_H(x, eps))
+
+
+def delta(x, eps):
+    return float(lib().orc_delta(x, eps))
+
+
+def delta_prime(x, eps):
+    return float(lib().orc_delta_prime(x, eps))
+
+
+def h(x, eps, l):
+    return float(lib().orc_h(x, eps, l))
+
+
+def h_prime(x, eps, l):
+    return float(lib().orc_h_prime(x, eps, l))
+
+
+# fields ---------------------------------------------------------------
+def grad(phi):
+    phi = _d(phi)
+    M, N = phi.shape
+    g1, g2 = np.empty_like(phi), np.empty_like(phi)
+    lib().orc_grad(M, N, _ptr(phi), _ptr(g1), _ptr(g2))
+    return g1, g2
+
+
+def div(u1, u2):
+    u1, u2 = _d(u1), _d(u2)
+    M, N = u1.shape
+    out = np.empty_like(u1)
+    lib().orc_div(M, N, _ptr(u1), _ptr(u2), _ptr(out))
+    return out
+
+
+def edge(f, sigma=1.0, rho=1.0, s=2):
+    f = _d(f)
+    M, N = f.shape
+    g = np.empty_like(f)
+    lib().orc_edge(M, N, _ptr(f), sigma, rho, s, _ptr(g))
+    return g
+
+
+def fft(x, inverse=False):
+    x = np.asarray(x, dtype=np.complex128)
+    re, im = _d(x.real.copy()), _d(x.imag.copy())
+    if lib().orc_fft(len(x), _ptr(re), _ptr(im), int(inverse)) != 0:
+        raise ValueError("length must be a power of two")
+    return re + 1j * im
+
+
+def fft2(x, inverse=False):
+    x = np.asarray(x, dtype=np.complex128)
+    M, N = x.shape
+    re, im = _d(x.real.copy()), _d(x.imag.copy())
+    if lib().orc_fft2(M, N, _ptr(re), _ptr(im), int(inverse)) != 0:
+        raise ValueError("sizes must be powers of two")
+    return re + 1j * im
+
+
+def symbol(M, N, tau, mu, k1, k2):
+    return float(lib().orc_symbol(M, N, tau, mu, k1, k2))
+
+
+def solve(F, tau, mu, check=True):
+    F = _d(F)
+    M, N = F.shape
+    phi = np.empty_like(F)
+    bad = lib().orc_solve(M, N, tau, mu, _ptr(F), _ptr(phi))
+    if check and bad:
+        raise FloatingPointError("imaginary part of the solve exceeds 1e-12 max|F| (Q11)")
+    return phi
+
+
+def window_sum(u1, u2, R, d, shape=0):
+    u1, u2 = _d(u1), _d(u2)
+    M, N = u1.shape
+    v1, v2 = np.empty_like(u1), np.empty_like(u1)
+    lib().orc_window_sum(M, N, R, d, shape, _ptr(u1), _ptr(u2), _ptr(v1), _ptr(v2))
+    return v1, v2
+
+
+def rhs(p, psi, w1, w2, b1, b2, g):
+    psi, w1, w2, b1, b2, g = map(_d, (psi, w1, w2, b1, b2, g))
+    M, N = psi.shape
+    F = np.empty_like(psi)
+    lib().orc_rhs(M, N, _P(p), _ptr(psi), _ptr(w1), _ptr(w2), _ptr(b1), _ptr(b2), _ptr(g), _ptr(F))
+    return F
+
+
+def shrink(B1, B2, t):
+    o1, o2 = C.c_double(), C.c_double()
+    lib().orc_shrink(B1, B2, t, C.byref(o1), C.byref(o2))
+    return o1.value, o2.value
+
+
+def project(mode, a1, a2):
+    o1, o2 = C.c_double(), C.c_double()
+    lib().orc_project(mode, a1, a2, C.byref(o1), C.byref(o2))
+    return o1.value, o2.value
+
+
+def wb(p, phi, w1, w2, b1, b2, g):
+    """Returns new (w1, w2, b1, b2); inputs are not modified."""
+    phi, g = _d(phi), _d(g)
+    w1, w2, b1, b2 = (np.array(a, dtype=np.float64, copy=True) for a in (w1, w2, b1, b2))
+    M, N = phi.shape
+    lib().orc_wb(M, N, _P(p), _ptr(phi), _ptr(w1), _ptr(w2), _ptr(b1), _ptr(b2), _ptr(g))
+    return w1, w2, b1, b2
+
+
+def init(phi0):
+    phi0 = _d(phi0)
+    M, N = phi0.shape
+    out = [np.empty_like(phi0) for _ in range(5)]
+    lib().orc_init(M, N, _ptr(phi0), *[_ptr(a) for a in out])
+    return dict(phi=out[0], w1=out[1], w2=out[2], b1=out[3], b2=out[4])
+
+
+def sweep(p, psi, w1, w2, b1, b2, g):
+    psi = np.array(psi, dtype=np.float64, copy=True)
+    w1, w2, b1, b2, g = map(_d, (w1, w2, b1, b2, g))
+    M, N = psi.shape
+    bad = lib().orc_sweep(M, N, _P(p), _ptr(psi), _ptr(w1), _ptr(w2), _ptr(b1), _ptr(b2), _ptr(g))
+    if bad:
+        raise FloatingPointError("imaginary part of the solve exceeds tolerance (Q11)")
+    return psi
+
+
+def iterate(p, state, g, K):
+    """Advance `state` (dict phi, w1, w2, b1, b2 of float64 arrays) by K outer iterations, in place."""
+    g = _d(g)
+    for k in ("phi", "w1", "w2", "b1", "b2"):
+        state[k] = np.array(state[k], dtype=np.float64, copy=True, order="C")
+    M, N = g.shape
+    bad = lib().orc_iterate(M, N, _P(p), *[_ptr(state[k]) for k in ("phi", "w1", "w2", "b1", "b2")], _ptr(g), K)
+    if bad:
+        raise FloatingPointError(f"{bad} solves failed the imaginary-part check (Q11)")
+    return state
+
+
+def label(mask, conn=4):
+    m = np.ascontiguousarray(mask, dtype=np.uint8)
+    M, N = m.shape
+    lab = np.empty((M, N), dtype=np.int32)
+    n = lib().orc_label(M, N, _ptr(m), conn, _ptr(lab))
+    return int(n), lab
+
+
+def run(p, image, phi0, K):
+    """Algorithm 1 from scratch for one image: g (Eq. 1), init, K iterations."""
+    g = edge(image, p["sigma"], p["rho"], p["s"])
+    st = init(phi0)
+    iterate(p, st, g, K)
+    st["g"] = g
+    return st

@@ -1,0 +1,499 @@
+/*
+ * sr_oracle.c -- plain, slow, float64 CPU oracle for the Split Bregman
+ * Self-repelling Snake iteration (Pan et al., arXiv 2003.12693).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.
+ * It shares no code, header, table or constant generator with the CUDA
+ * path (paper_2003_12693_b200/csrc); neither includes the other.
+ *
+ * Citations: "P:n" is line n of PAPER.md (the LaTeX source); equation numbers
+ * are LaTeX's.  Readings of the paper where it is silent or garbled are the
+ * "Q" items of DESIGN.md §2 (= SURVEY.md §8(c)).
+ *
+ * Everything is written in the paper's order and notation, without blocking,
+ * fusion or reordering:
+ *   - regularizers: Eq. (5), (6), (29), (11), (28);
+ *   - stencils: Eq. (35), (36) as the Neumann-adjoint pair (Q6);
+ *   - edge indicator: Eq. (1) with a normalized Gaussian of radius ceil(3 sigma) (Q16);
+ *   - FFT: recursive radix-2 complex DFT, unnormalized forward, 1/n inverse;
+ *   - phi solve: Eq. (31)-(33), full complex 2-D FFT, divide by the symbol of Eq. (32) (Q10);
+ *   - window sum: the direct double loop of P:368 (disc or square window, Q2, Q5);
+ *   - RHS: Eq. (37) with phi^{k+1,s} in every term (Q8);
+ *   - w/b update: Eq. (41), (42), projection Eq. (40) as BALL/SPHERE/NONE (Q1), Eq. (23);
+ *   - fixed-point w update: Eq. (38)-(40) (NEXT-2);
+ *   - Algorithm 1 with fixed S sweeps (Q7) and the north-star clamp (Q9);
+ *   - connected-component labelling by flood fill (validation).
+ *
+ * Parity pins: every function is pinned by tests/test_oracle_*.py against
+ * closed forms, brute force, numpy/scipy library routines or invariants
+ * (DESIGN.md §4).  No function here is "parity unpinned".
+ *
+ * Compiled with -O2 -ffp-contract=off (no FMA contraction, no fast-math).
+ * OpenMP parallelises only independent per-pixel / per-row loops, so results
+ * are bitwise deterministic regardless of the thread count.
+ */
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#ifndef M_PI
+#define M_PI 3.14159265358979323846
+#endif
+
+typedef struct {
+    double gamma, alpha, beta, mu;   /* Eq. (7), (22) weights */
+    double epsilon, l;               /* Eq. (5)-(6) half-width; Eq. (11) band offset */
+    double d;                        /* Eq. (10)/(38) Gaussian scale */
+    int window;                      /* summation radius R of P:368 (BASELINE's "l") */
+    int window_shape;                /* 0 = disc p^2+q^2 <= R^2, 1 = square |p|,|q| <= R */
+    double tau;                      /* Eq. (30)/(37) time step */
+    int S;                           /* phi sweeps per outer iteration (Q7) */
+    double phi_clip;                 /* >0: clamp phi^{k+1} to [-phi_clip, phi_clip] (Q9) */
+    int w_proj;                      /* 0 BALL, 1 SPHERE, 2 NONE (Q1) */
+    int w_mode;                      /* 0 threshold Eq. (41)-(42); 1 fixed point Eq. (38)-(39) */
+    int w_iters;                     /* fixed-point sweeps r = 0..w_iters-1 */
+} orc_params;
+
+#define IDX(i, j) ((size_t)(i) * (size_t)N + (size_t)(j))
+
+/* ------------------------------------------------------------------ */
+/* Regularizers                                                        */
+/* ------------------------------------------------------------------ */
+
+/* Eq. (5) */
+double orc_H(double phi, double eps)
+{
+    if (phi > eps) return 1.0;
+    if (phi < -eps) return 0.0;
+    return 0.5 * (1.0 + phi / eps + sin(M_PI * phi / eps) / M_PI);
+}
+
+/* Eq. (6) */
+double orc_delta(double phi, double eps)
+{
+    if (fabs(phi) > eps) return 0.0;
+    return (1.0 + cos(M_PI * phi / eps)) / (2.0 * eps);
+}
+
+/* Eq. (29) */
+double orc_delta_prime(double phi, double eps)
+{
+    if (fabs(phi) > eps) return 0.0;
+    return -(M_PI / (2.0 * eps * eps)) * sin(M_PI * phi / eps);
+}
+
+/* Eq. (11): h = H(phi + l) (1 - H(phi - l)) */
+double orc_h(double phi, double eps, double l)
+{
+    return orc_H(phi + l, eps) * (1.0 - orc_H(phi - l, eps));
+}
+
+/* Eq. (28): h' = delta(phi + l)(1 - H(phi - l)) - H(phi + l) delta(phi - l) */
+double orc_h_prime(double phi, double eps, double l)
+{
+    return orc_delta(phi + l, eps) * (1.0 - orc_H(phi - l, eps))
+         - orc_H(phi + l, eps) * orc_delta(phi - l, eps);
+}
+
+/* ------------------------------------------------------------------ */
+/* Stencils, Eq. (35)-(36) as the exact adjoint pair (reading Q6)      */
+/* ------------------------------------------------------------------ */
+
+/* Eq. (35): forward differences; zero on the last row / last column. */
+void orc_grad(int M, int N, const double *phi, double *g1, double *g2)
+{
+    #pragma omp parallel for schedule(static)
+    for (int i = 0; i < M; i++)
+        for (int j = 0; j < N; j++) {
+            g1[IDX(i, j)] = (i < M - 1) ? phi[IDX(i + 1, j)] - phi[IDX(i, j)] : 0.0;
+            g2[IDX(i, j)] = (j < N - 1) ? phi[IDX(i, j + 1)] - phi[IDX(i, j)] : 0.0;
+        }
+}
+
+/* Eq. (36): backward differences; u1 is dropped on the last row and u2 on
+ * the last column (where grad is defined as 0), out-of-range terms are 0. */
+void orc_div(int M, int N, const double *u1, const double *u2, double *out)
+{
+    #pragma omp parallel for schedule(static)
+    for (int i = 0; i < M; i++)
+        for (int j = 0; j < N; j++) {
+            double s = 0.0;
+            if (i < M - 1) s += u1[IDX(i, j)];
+            if (i > 0) s -= u1[IDX(i - 1, j)];
+            if (j < N - 1) s += u2[IDX(i, j)];
+            if (j > 0) s -= u2[IDX(i, j - 1)];
+            out[IDX(i, j)] = s;
+        }
+}
+
+/* ------------------------------------------------------------------ */
+/* Edge indicator, Eq. (1)                                    */
+/* ------------------------------------------------------------------ */
+
+/* g = 1 / (1 + rho |grad(G_sigma * f)|^s); G_sigma: normalized Gaussian
+ * exp(-t^2/(2 sigma^2)), t = -r..r, r = ceil(3 sigma), separable rows then
+ * columns with replicate padding (Q16); grad by central differences with
+ * replicate padding. */
+void orc_edge(int M, int N, const double *f, double sigma, double rho, int s, double *g)
+{
+    int r = (int)ceil(3.0 * sigma);
+    double *k = (double *)malloc(sizeof(double) * (2 * r + 1));
+    double ks = 0.0;
+    for (int t = -r; t <= r; t++) { k[t + r] = exp(-(double)(t * t) / (2.0 * sigma * sigma)); ks += k[t + r]; }
+    for (int t = 0; t <= 2 * r; t++) k[t] /= ks;
+    double *tmp = (double *)malloc(sizeof(double) * (size_t)M * N);
+    double *fs = (double *)malloc(sizeof(double) * (size_t)M * N);
+    /* rows: convolve along j */
+    #pragma omp parallel for schedule(static)
+    for (int i = 0; i < M; i++)
+        for (int j = 0; j < N; j++) {
+            double a = 0.0;
+            for (int t = -r; t <= r; t++) {
+                int jj = j + t; if (jj < 0) jj = 0; if (jj > N - 1) jj = N - 1;
+                a += k[t + r] * f[IDX(i, jj)];
+            }
+            tmp[IDX(i, j)] = a;
+        }
+    /* columns: convolve along i */
+    #pragma omp parallel for schedule(static)
+    for (int i = 0; i < M; i++)
+        for (int j = 0; j < N; j++) {
+            double a = 0.0;
+            for (int t = -r; t <= r; t++) {
+                int ii = i + t; if (ii < 0) ii = 0; if (ii > M - 1) ii = M - 1;
+                a += k[t + r] * tmp[IDX(ii, j)];
+            }
+            fs[IDX(i, j)] = a;
+        }
+    #pragma omp parallel for schedule(static)
+    for (int i = 0; i < M; i++)
+        for (int j = 0; j < N; j++) {
+            int ip = i + 1 < M ? i + 1 : M - 1, im = i > 0 ? i - 1 : 0;
+            int jp = j + 1 < N ? j + 1 : N - 1, jm = j > 0 ? j - 1 : 0;
+            double gx = (fs[IDX(ip, j)] - fs[IDX(im, j)]) / 2.0;
+            double gy = (fs[IDX(i, jp)] - fs[IDX(i, jm)]) / 2.0;
+            double m2 = gx * gx + gy * gy;
+            double mag = (s == 2) ? m2 : sqrt(m2);
+            g[IDX(i, j)] = 1.0 / (1.0 + rho * mag);
+        }
+    free(k); free(tmp); free(fs);
+}
+
+/* ------------------------------------------------------------------ */
+/* FFT: recursive radix-2, X[k] = sum_n x[n] exp(-2 pi i k n / n)      */
+/* ------------------------------------------------------------------ */
+
+static void fft_rec(int n, double *re, double *im, int stride, double *ore, double *oim, int sign)
+{
+    if (n == 1) { ore[0] = re[0]; oim[0] = im[0]; return; }
+    int h = n / 2;
+    /* even samples -> first half of the output, odd samples -> second half */
+    fft_rec(h, re, im, 2 * stride, ore, oim, sign);
+    fft_rec(h, re + stride, im + stride, 2 * stride, ore + h, oim + h, sign);
+    for (int k = 0; k < h; k++) {
+        double a = sign * 2.0 * M_PI * (double)k / (double)n;
+        double c = cos(a), s = sin(a);
+        double er = ore[k], ei = oim[k];
+        double orr = ore[k + h], oi = oim[k + h];
+        double tr = c * orr - s * oi, ti = c * oi + s * orr;
+        ore[k] = er + tr;  oim[k] = ei + ti;
+        ore[k + h] = er - tr;  oim[k + h] = ei - ti;
+    }
+}
+
+/* In place; n a power of two; inverse = 1 gives (1/n) sum x[k] exp(+2 pi i k n / n). */
+int orc_fft(int n, double *re, double *im, int inverse)
+{
+    if (n < 1 || (n & (n - 1))) return -1;
+    double *xr = (double *)malloc(sizeof(double) * n), *xi = (double *)malloc(sizeof(double) * n);
+    memcpy(xr, re, sizeof(double) * n); memcpy(xi, im, sizeof(double) * n);
+    fft_rec(n, xr, xi, 1, re, im, inverse ? +1 : -1);
+    if (inverse) for (int k = 0; k < n; k++) { re[k] /= n; im[k] /= n; }
+    free(xr); free(xi);
+    return 0;
+}
+
+/* 2-D FFT of an M x N complex array: rows, then columns. */
+int orc_fft2(int M, int N, double *re, double *im, int inverse)
+{
+    if (M < 1 || N < 1 || (M & (M - 1)) || (N & (N - 1))) return -1;
+    #pragma omp parallel for schedule(static)
+    for (int i = 0; i < M; i++) orc_fft(N, re + IDX(i, 0), im + IDX(i, 0), inverse);
+    #pragma omp parallel
+    {
+        double *cr = (double *)malloc(sizeof(double) * M), *ci = (double *)malloc(sizeof(double) * M);
+        #pragma omp for schedule(static)
+        for (int j = 0; j < N; j++) {
+            for (int i = 0; i < M; i++) { cr[i] = re[IDX(i, j)]; ci[i] = im[IDX(i, j)]; }
+            orc_fft(M, cr, ci, inverse);
+            for (int i = 0; i < M; i++) { re[IDX(i, j)] = cr[i]; im[IDX(i, j)] = ci[i]; }
+        }
+        free(cr); free(ci);
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* phi sub-problem, Eq. (31)-(33)                           */
+/* ------------------------------------------------------------------ */
+
+/* Symbol of (1 - tau mu Delta) under the periodic DFT, Eq. (32) with the
+ * garbled bracket read as 1 - tau mu (2 cos z1 + 2 cos z2 - 4) (Q10),
+ * z1 = 2 pi k1 / M, z2 = 2 pi k2 / N, 0-based k. */
+double orc_symbol(int M, int N, double tau, double mu, int k1, int k2)
+{
+    double z1 = 2.0 * M_PI * (double)k1 / (double)M;
+    double z2 = 2.0 * M_PI * (double)k2 / (double)N;
+    return 1.0 - tau * mu * (2.0 * cos(z1) + 2.0 * cos(z2) - 4.0);
+}
+
+/* phi = Re F^{-1}( F(F) / symbol ), Eq. (33).  Returns 1 if the discarded
+ * imaginary part exceeds 1e-12 max|F| (Q11), else 0. */
+int orc_solve(int M, int N, double tau, double mu, const double *F, double *phi)
+{
+    size_t n = (size_t)M * N;
+    double *re = (double *)malloc(sizeof(double) * n), *im = (double *)calloc(n, sizeof(double));
+    memcpy(re, F, sizeof(double) * n);
+    orc_fft2(M, N, re, im, 0);
+    for (int k1 = 0; k1 < M; k1++)
+        for (int k2 = 0; k2 < N; k2++) {
+            double sg = orc_symbol(M, N, tau, mu, k1, k2);
+            re[IDX(k1, k2)] /= sg;
+            im[IDX(k1, k2)] /= sg;
+        }
+    orc_fft2(M, N, re, im, 1);
+    double fmax = 0.0, imax = 0.0;
+    for (size_t q = 0; q < n; q++) {
+        if (fabs(F[q]) > fmax) fmax = fabs(F[q]);
+        if (fabs(im[q]) > imax) imax = fabs(im[q]);
+        phi[q] = re[q];
+    }
+    free(re); free(im);
+    return imax > 1e-12 * (fmax > 0 ? fmax : 1.0) ? 1 : 0;
+}
+
+/* ------------------------------------------------------------------ */
+/* Non-local window sum, P:368-369 (and Eq. 38)                        */
+/* ------------------------------------------------------------------ */
+
+/* v(i,j) = sum_{(p,q) in W} exp(-(p^2+q^2)/d^2) u(i+p, j+q); terms outside
+ * the image are 0 (Q5).  W: disc p^2+q^2 <= R^2 (shape 0) or square (1). */
+void orc_window_sum(int M, int N, int R, double d, int shape,
+                    const double *u1, const double *u2, double *v1, double *v2)
+{
+    #pragma omp parallel for schedule(static)
+    for (int i = 0; i < M; i++)
+        for (int j = 0; j < N; j++) {
+            double a1 = 0.0, a2 = 0.0;
+            for (int p = -R; p <= R; p++)
+                for (int q = -R; q <= R; q++) {
+                    if (shape == 0 && p * p + q * q > R * R) continue;
+                    int ii = i + p, jj = j + q;
+                    if (ii < 0 || ii >= M || jj < 0 || jj >= N) continue;
+                    double G = exp(-(double)(p * p + q * q) / (d * d));
+                    a1 += G * u1[IDX(ii, jj)];
+                    a2 += G * u2[IDX(ii, jj)];
+                }
+            v1[IDX(i, j)] = a1;
+            v2[IDX(i, j)] = a2;
+        }
+}
+
+/* ------------------------------------------------------------------ */
+/* RHS of the phi sweep, Eq. (37)                           */
+/* ------------------------------------------------------------------ */
+
+/* F = psi + tau [ -gamma g |w| delta'(psi) + alpha g delta(psi)
+ *                 + 2 beta h'(psi) w . v + mu div(b - w) ],
+ * v = window_sum(h(psi) w) (with phi^{k+1,s} = psi, Q8). */
+void orc_rhs(int M, int N, const orc_params *P, const double *psi,
+             const double *w1, const double *w2, const double *b1, const double *b2,
+             const double *g, double *F)
+{
+    size_t n = (size_t)M * N;
+    double *u1 = malloc(sizeof(double) * n), *u2 = malloc(sizeof(double) * n);
+    double *v1 = malloc(sizeof(double) * n), *v2 = malloc(sizeof(double) * n);
+    double *c1 = malloc(sizeof(double) * n), *c2 = malloc(sizeof(double) * n);
+    double *dv = malloc(sizeof(double) * n);
+    for (size_t q = 0; q < n; q++) {
+        double hq = orc_h(psi[q], P->epsilon, P->l);
+        u1[q] = hq * w1[q];
+        u2[q] = hq * w2[q];
+        c1[q] = b1[q] - w1[q];
+        c2[q] = b2[q] - w2[q];
+    }
+    orc_window_sum(M, N, P->window, P->d, P->window_shape, u1, u2, v1, v2);
+    orc_div(M, N, c1, c2, dv);
+    #pragma omp parallel for schedule(static)
+    for (size_t q = 0; q < n; q++) {
+        double wn = sqrt(w1[q] * w1[q] + w2[q] * w2[q]);
+        double t = -P->gamma * g[q] * wn * orc_delta_prime(psi[q], P->epsilon)
+                 + P->alpha * g[q] * orc_delta(psi[q], P->epsilon)
+                 + 2.0 * P->beta * orc_h_prime(psi[q], P->epsilon, P->l) * (w1[q] * v1[q] + w2[q] * v2[q])
+                 + P->mu * dv[q];
+        F[q] = psi[q] + P->tau * t;
+    }
+    free(u1); free(u2); free(v1); free(v2); free(c1); free(c2); free(dv);
+}
+
+/* ------------------------------------------------------------------ */
+/* w sub-problem                                                       */
+/* ------------------------------------------------------------------ */
+
+/* Generalized soft threshold, Eq. (42), with 0 * 0/|0| = 0. */
+void orc_shrink(double B1, double B2, double t, double *o1, double *o2)
+{
+    double nb = sqrt(B1 * B1 + B2 * B2);
+    if (nb > 0.0) {
+        double m = nb - t; if (m < 0.0) m = 0.0;
+        *o1 = m * B1 / nb;
+        *o2 = m * B2 / nb;
+    } else {
+        *o1 = 0.0; *o2 = 0.0;
+    }
+}
+
+/* Projection, Eq. (40), "used afterwards" P:400; modes per Q1. */
+void orc_project(int mode, double a1, double a2, double *o1, double *o2)
+{
+    double n = sqrt(a1 * a1 + a2 * a2);
+    if (mode == 0) {                       /* BALL: w / max(1, |w|) */
+        double s = n > 1.0 ? n : 1.0;
+        *o1 = a1 / s; *o2 = a2 / s;
+    } else if (mode == 1) {                /* SPHERE: w / |w| where |w| > 1e-4 */
+        if (n > 1e-4) { *o1 = a1 / n; *o2 = a2 / n; } else { *o1 = a1; *o2 = a2; }
+    } else {                               /* NONE */
+        *o1 = a1; *o2 = a2;
+    }
+}
+
+/* w^{k+1} by Eq. (41)-(42) (w_mode 0) or the fixed point Eq. (38)-(39)
+ * (w_mode 1), projected (Eq. 40), then b^{k+1} = b^k + grad phi^{k+1} - w^{k+1}
+ * (Eq. 23).  phi is phi^{k+1}; w, b hold w^k, b^k on entry. */
+void orc_wb(int M, int N, const orc_params *P, const double *phi,
+            double *w1, double *w2, double *b1, double *b2, const double *g)
+{
+    size_t n = (size_t)M * N;
+    double *gp1 = malloc(sizeof(double) * n), *gp2 = malloc(sizeof(double) * n);
+    double *u1 = malloc(sizeof(double) * n), *u2 = malloc(sizeof(double) * n);
+    double *v1 = malloc(sizeof(double) * n), *v2 = malloc(sizeof(double) * n);
+    double *hh = malloc(sizeof(double) * n);
+    double *n1 = malloc(sizeof(double) * n), *n2 = malloc(sizeof(double) * n);
+    orc_grad(M, N, phi, gp1, gp2);
+    for (size_t q = 0; q < n; q++) hh[q] = orc_h(phi[q], P->epsilon, P->l);
+    if (P->w_mode == 0) {
+        /* Eq. (41): B = grad phi^{k+1} + b^k + (2 beta/mu) h(phi^{k+1}) sum G w^k h(phi^{k+1}) */
+        for (size_t q = 0; q < n; q++) { u1[q] = hh[q] * w1[q]; u2[q] = hh[q] * w2[q]; }
+        orc_window_sum(M, N, P->window, P->d, P->window_shape, u1, u2, v1, v2);
+        for (size_t q = 0; q < n; q++) {
+            double B1 = gp1[q] + b1[q] + (2.0 * P->beta / P->mu) * hh[q] * v1[q];
+            double B2 = gp2[q] + b2[q] + (2.0 * P->beta / P->mu) * hh[q] * v2[q];
+            double t = (P->gamma / P->mu) * g[q] * orc_delta(phi[q], P->epsilon);
+            double s1, s2;
+            orc_shrink(B1, B2, t, &s1, &s2);
+            orc_project(P->w_proj, s1, s2, &n1[q], &n2[q]);
+        }
+    } else {
+        /* Eq. (38)-(39): w^{k+1,0} = w^k; w~^{r+1} = (mu grad phi + mu b + 2 beta h v^r)/(gamma g delta + mu) */
+        memcpy(n1, w1, sizeof(double) * n); memcpy(n2, w2, sizeof(double) * n);
+        for (int r = 0; r < P->w_iters; r++) {
+            for (size_t q = 0; q < n; q++) { u1[q] = hh[q] * n1[q]; u2[q] = hh[q] * n2[q]; }
+            orc_window_sum(M, N, P->window, P->d, P->window_shape, u1, u2, v1, v2);
+            for (size_t q = 0; q < n; q++) {
+                double den = P->gamma * g[q] * orc_delta(phi[q], P->epsilon) + P->mu;
+                double a1 = (P->mu * gp1[q] + P->mu * b1[q] + 2.0 * P->beta * hh[q] * v1[q]) / den;
+                double a2 = (P->mu * gp2[q] + P->mu * b2[q] + 2.0 * P->beta * hh[q] * v2[q]) / den;
+                orc_project(P->w_proj, a1, a2, &n1[q], &n2[q]);
+            }
+        }
+    }
+    for (size_t q = 0; q < n; q++) {
+        b1[q] = b1[q] + gp1[q] - n1[q];
+        b2[q] = b2[q] + gp2[q] - n2[q];
+        w1[q] = n1[q];
+        w2[q] = n2[q];
+    }
+    free(gp1); free(gp2); free(u1); free(u2); free(v1); free(v2); free(hh); free(n1); free(n2);
+}
+
+/* ------------------------------------------------------------------ */
+/* Algorithm 1                                              */
+/* ------------------------------------------------------------------ */
+
+/* Initialization (1): phi = phi0, w^0 = grad phi^0 (Q12), b^0 = 0. */
+void orc_init(int M, int N, const double *phi0, double *phi, double *w1, double *w2, double *b1, double *b2)
+{
+    size_t n = (size_t)M * N;
+    memcpy(phi, phi0, sizeof(double) * n);
+    orc_grad(M, N, phi0, w1, w2);
+    memset(b1, 0, sizeof(double) * n);
+    memset(b2, 0, sizeof(double) * n);
+}
+
+/* One sweep: psi <- solve(rhs(psi)).  Returns the solve's imaginary-part flag. */
+int orc_sweep(int M, int N, const orc_params *P, double *psi, const double *w1, const double *w2,
+              const double *b1, const double *b2, const double *g)
+{
+    size_t n = (size_t)M * N;
+    double *F = malloc(sizeof(double) * n);
+    orc_rhs(M, N, P, psi, w1, w2, b1, b2, g, F);
+    int bad = orc_solve(M, N, P->tau, P->mu, F, psi);
+    free(F);
+    return bad;
+}
+
+/* K outer iterations (2) of Algorithm 1 with S sweeps each (Q7), the clamp
+ * of phi^{k+1} after the last sweep (Q9), then w (Eq. 42 / 39, 40) and b (Eq. 23).
+ * Returns the number of solves whose imaginary-part check failed. */
+int orc_iterate(int M, int N, const orc_params *P, double *phi, double *w1, double *w2,
+                double *b1, double *b2, const double *g, int K)
+{
+    int bad = 0;
+    size_t n = (size_t)M * N;
+    for (int k = 0; k < K; k++) {
+        for (int s = 0; s < P->S; s++) bad += orc_sweep(M, N, P, phi, w1, w2, b1, b2, g);
+        if (P->phi_clip > 0.0)
+            for (size_t q = 0; q < n; q++) {
+                if (phi[q] > P->phi_clip) phi[q] = P->phi_clip;
+                if (phi[q] < -P->phi_clip) phi[q] = -P->phi_clip;
+            }
+        orc_wb(M, N, P, phi, w1, w2, b1, b2, g);
+    }
+    return bad;
+}
+
+/* ------------------------------------------------------------------ */
+/* Validation: connected components of a mask by flood fill            */
+/* ------------------------------------------------------------------ */
+
+/* labels[q] = 0 for background, 1..count for components; conn = 4 or 8. */
+int orc_label(int M, int N, const unsigned char *mask, int conn, int *labels)
+{
+    size_t n = (size_t)M * N;
+    int *stack = (int *)malloc(sizeof(int) * n);
+    int count = 0;
+    for (size_t q = 0; q < n; q++) labels[q] = 0;
+    for (size_t q0 = 0; q0 < n; q0++) {
+        if (!mask[q0] || labels[q0]) continue;
+        count++;
+        size_t top = 0;
+        stack[top++] = (int)q0;
+        labels[q0] = count;
+        while (top) {
+            int q = stack[--top];
+            int i = q / N, j = q % N;
+            for (int di = -1; di <= 1; di++)
+                for (int dj = -1; dj <= 1; dj++) {
+                    if (!di && !dj) continue;
+                    if (conn == 4 && di && dj) continue;
+                    int ii = i + di, jj = j + dj;
+                    if (ii < 0 || ii >= M || jj < 0 || jj >= N) continue;
+                    size_t r = IDX(ii, jj);
+                    if (mask[r] && !labels[r]) { labels[r] = count; stack[top++] = (int)r; }
+                }
+        }
+    }
+    free(stack);
+    return count;
+}

@@ -1,0 +1,132 @@
+"""Pins of the oracle's whole iteration (Algorithm 1): fixed points, metamorphic
+symmetries, clamp, determinism, and topology behaviour (north star / BASELINE configs[0])."""
+import numpy as np
+import pytest
+
+
+def _run(orc, P, phi0, g, K):
+    st = orc.init(phi0)
+    orc.iterate(P, st, g, K)
+    return st
+
+
+def test_plateau_fixed_point(orc):
+    """phi = +-1 plateaus with w = b = 0 stay put: delta, delta', h' vanish there (eps = l = 1/2)."""
+    from synth import paper_params
+    P = paper_params(3)
+    phi = np.ones((16, 16))
+    st = dict(phi=phi.copy(), w1=np.zeros_like(phi), w2=np.zeros_like(phi), b1=np.zeros_like(phi), b2=np.zeros_like(phi))
+    orc.iterate(P, st, np.full_like(phi, 0.5), 3)
+    assert np.allclose(st["phi"], 1.0, atol=1e-14)
+    assert np.allclose(st["w1"], 0, atol=1e-14) and np.allclose(st["b1"], 0, atol=1e-14)
+
+
+def test_smooth_fixed_point(orc):
+    """beta = gamma = alpha = 0, b = 0, w = grad phi, phi smooth with |phi|, |grad phi| <= 1 and a
+    constant frame: the mu terms cancel in F, shrink (t = 0) and BALL keep w = grad phi, b stays 0."""
+    from synth import paper_params
+    P = paper_params(3, beta=0.0, gamma=0.0, alpha=0.0)
+    M = N = 32
+    ii, jj = np.meshgrid(np.arange(M), np.arange(N), indexing="ij")
+    phi = 0.5 * np.exp(-((ii - 15.5) ** 2 + (jj - 15.5) ** 2) / 30.0)
+    phi[:3] = phi[-3:] = 0.0
+    phi[:, :3] = phi[:, -3:] = 0.0
+    phi[3:-3, 3:-3] = phi[3:-3, 3:-3] - phi[3, 3]
+    st = _run(orc, P, phi, np.ones((M, N)), 2)
+    assert np.allclose(st["phi"], phi, atol=1e-12)
+    g1, g2 = orc.grad(phi)
+    assert np.allclose(st["w1"], g1, atol=1e-12) and np.allclose(st["b1"], 0, atol=1e-12)
+
+
+def test_sign_flip_metamorphic(orc):
+    """(phi, w, b, alpha) -> (-phi, -w, -b, -alpha) maps the iteration onto itself (reading Q3)."""
+    from synth import make_config
+    c = make_config("c1")
+    P = c["params"]
+    g = orc.edge(c["image"][0], P["sigma"], P["rho"], P["s"])
+    a = _run(orc, P, c["phi0"][0], g, 5)
+    Pm = dict(P, alpha=-P["alpha"])
+    b = _run(orc, Pm, -c["phi0"][0], g, 5)
+    for k in ("phi", "w1", "w2", "b1", "b2"):
+        assert np.allclose(a[k], -b[k], atol=1e-10), k
+
+
+def test_transpose_metamorphic(orc):
+    """M = N: transposing (i, j) and swapping (w1, w2), (b1, b2) commutes with the iteration."""
+    from synth import make_config
+    c = make_config("c1")
+    P = c["params"]
+    img = c["image"][0]
+    g = orc.edge(img, P["sigma"], P["rho"], P["s"])
+    gT = orc.edge(img.T.copy(), P["sigma"], P["rho"], P["s"])
+    assert np.allclose(g.T, gT, atol=1e-14)
+    a = _run(orc, P, c["phi0"][0], g, 4)
+    b = _run(orc, P, c["phi0"][0].T.copy(), gT, 4)
+    assert np.allclose(a["phi"], b["phi"].T, atol=1e-10)
+    assert np.allclose(a["w1"], b["w2"].T, atol=1e-10) and np.allclose(a["b2"], b["b1"].T, atol=1e-10)
+
+
+def test_tau_zero_leaves_phi(orc):
+    from synth import make_config
+    c = make_config("c1")
+    P = dict(c["params"], tau=0.0)
+    g = orc.edge(c["image"][0], 1.0, P["rho"], 2)
+    st = _run(orc, P, c["phi0"][0], g, 3)
+    assert np.allclose(st["phi"], c["phi0"][0], atol=1e-14)
+
+
+def test_clamp_and_determinism(orc):
+    from synth import make_config
+    c = make_config("c1")
+    P = c["params"]
+    g = orc.edge(c["image"][0], 1.0, P["rho"], 2)
+    a = _run(orc, P, c["phi0"][0], g, 8)
+    b = _run(orc, P, c["phi0"][0], g, 8)
+    assert np.all(np.abs(a["phi"]) <= 1.0)                 # north star: phi inside [-1, 1]
+    for k in a:
+        assert np.array_equal(a[k], b[k])                  # bitwise deterministic
+
+
+def test_label_vs_scipy(orc):
+    from scipy.ndimage import label
+    rng = np.random.default_rng(0)
+    for _ in range(5):
+        m = rng.random((40, 33)) < 0.45
+        n4, l4 = orc.label(m, 4)
+        r4, k4 = label(m)
+        n8, _ = orc.label(m, 8)
+        r8, k8 = label(m, structure=np.ones((3, 3)))
+        assert n4 == k4 and n8 == k8
+        # same partition (labels may be numbered differently)
+        assert len(set(zip(l4[m].tolist(), r4[m].tolist()))) == n4
+
+
+@pytest.mark.slow
+def test_c1_topology_sr_vs_gac(orc):
+    """BASELINE configs[0]: exactly one component of {phi_BJ > 0} = {phi < 0} after K = 300 (SR);
+    the beta = 0 control (plain GAC + balloon) does not keep the single component."""
+    from synth import make_config
+    c = make_config("c1")
+    P = c["params"]
+    g = orc.edge(c["image"][0], P["sigma"], P["rho"], P["s"])
+    sr = _run(orc, P, c["phi0"][0], g, c["K"])
+    assert orc.label(sr["phi"] < 0)[0] == 1
+    gac = _run(orc, dict(P, beta=0.0), c["phi0"][0], g, c["K"])
+    assert orc.label(gac["phi"] < 0)[0] != 1
+
+
+@pytest.mark.slow
+def test_two_seed_merge(orc):
+    """North star: two growing seeds (alpha < 0) that plain GAC (beta = 0) merges stay two
+    components under SR."""
+    from synth import make_config
+    c = make_config("c1")
+    P = dict(c["params"], alpha=-4.0)
+    ii, jj = np.meshgrid(np.arange(128.0), np.arange(128.0), indexing="ij")
+    seeds = ((ii - 63.5) ** 2 + (jj - 41.5) ** 2 <= 100) | ((ii - 63.5) ** 2 + (jj - 85.5) ** 2 <= 100)
+    phi0 = np.where(seeds, -1.0, 1.0)
+    g = orc.edge(c["image"][0], P["sigma"], P["rho"], P["s"])
+    sr = _run(orc, P, phi0, g, 300)
+    gac = _run(orc, dict(P, beta=0.0), phi0, g, 300)
+    assert orc.label(sr["phi"] < 0)[0] == 2
+    assert orc.label(gac["phi"] < 0)[0] == 1

@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""Benchmark of the Split Bregman SR iteration on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c3]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (one rank per GPU, NCCL)
+
+Workload: BASELINE configs[2] = C3, a batch of 64 independent 1024x1024 fp32
+images, 1000 Split Bregman iterations each, window radius 4 -- the config the metric's
+"1/2/4/8 B200" batch scaling and "% of HBM peak" are quoted on.  One STEP is the whole job
+for the batch: set_image (edge indicator Eq. 1 + init, §8(a) rows a0-a1) and 1000 outer
+iterations (rows a2-a5: 3 x [RHS Eq. 37 + FFT solve Eq. 33] + w/b update Eq. 41/42/40/23).
+With N GPUs the 64 images are sharded by image (no collective in the loop), so total work is
+fixed ("strong").  value = 64 * 1024^2 * 1000 * steps / (max over ranks of the device time) / 1e6.
+
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "megapixel-iterations/s per SB-SR iteration"
+UNIT = "Mpx-iter/s"
+# algorithmic HBM bytes per pixel per launch of each kernel class
+BYTES_PER_PX = {"rhs": 28.0, "rows_r2c": 8.0, "cols_solve": 8.0, "rows_c2r": 8.0, "wb": 40.0}
+MODEL_BYTES_PER_PX_ITER = 172.0   # SURVEY.md §8(d) fused model (S = 3)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--images", type=int, default=None, help="override the batch (C3 only)")
+    ap.add_argument("--iters", type=int, default=None, help="override iterations per step")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def workload(args):
+    from synth import CONFIGS
+    cfg = dict(CONFIGS[args.config])
+    if args.images:
+        cfg["batch"] = args.images
+    if args.iters:
+        cfg["K"] = args.iters
+    return cfg
+
+
+class ClockSampler:
+    """nvidia-smi equivalent via NVML, sampled during the timed region (B200_PROFILING.md clocks line)."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self._stop = threading.Event()
+        self.ok = True
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.ok = False
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and bit != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.1)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def cpu_baseline_oracle(cfg, target_s=12.0):
+    """The float64 oracle as it stands, on this host's cores, on a bounded sample of the workload:
+    one image of the config, as many iterations as fit ~target_s (at least 1)."""
+    import numpy as np
+    import oracle
+    from synth import make_config
+    cores = len(os.sched_getaffinity(0))
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    c = make_config(cfg["name"], images=[0]) if cfg["name"] == "c3" else make_config(cfg["name"])
+    p = c["params"]
+    img, phi0 = c["image"][0], c["phi0"][0]
+    M, N = img.shape
+    g = oracle.edge(img, p["sigma"], p["rho"], p["s"])
+    st = oracle.init(phi0)
+    t0 = time.perf_counter()
+    oracle.iterate(p, st, g, 1)
+    t1 = time.perf_counter() - t0
+    k = max(1, int(target_s / max(t1, 1e-3)) - 1)
+    t0 = time.perf_counter()
+    oracle.iterate(p, st, g, k)
+    t = time.perf_counter() - t0
+    k += 1
+    t += t1
+    del np
+    return {"value": M * N * k / t / 1e6, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"1 image of {cfg['name']} ({M}x{N}), {k} SB iterations, float64 C oracle, "
+                      f"OMP_NUM_THREADS={os.environ.get('OMP_NUM_THREADS')}, {t:.1f} s"}
+
+
+def run_reference(args, cfg, rank):
+    """--impl reference: the float64 CPU oracle, rank 0 only."""
+    if rank != 0:
+        return None
+    import oracle
+    from synth import make_config
+    oracle.build()
+    cores = len(os.sched_getaffinity(0))
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    c = make_config(cfg["name"], images=[0]) if cfg["name"] == "c3" else make_config(cfg["name"])
+    p = c["params"]
+    img, phi0 = c["image"][0], c["phi0"][0]
+    M, N = img.shape
+    g = oracle.edge(img, p["sigma"], p["rho"], p["s"])
+    st = oracle.init(phi0)
+    # each step: one outer iteration of one image (bounded sample of the workload)
+    for _ in range(args.warmup):
+        oracle.iterate(p, st, g, 1)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.iterate(p, st, g, 1)
+    t = time.perf_counter() - t0
+    value = M * N * args.steps / t / 1e6
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_json(cfg, args.gpus),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"each step = 1 SB iteration of image 0 of {cfg['name']} ({M}x{N}), "
+                                       f"float64 C oracle, OMP_NUM_THREADS={os.environ['OMP_NUM_THREADS']}"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def config_json(cfg, ngpu):
+    return {"workload": f"{cfg['name']}: {cfg['batch']} x {cfg['M']}x{cfg['N']} fp32 images, {cfg['K']} SB "
+                        f"iterations each, window radius {cfg['window']}, S=3",
+            "config_index": cfg["index"], "images": cfg["batch"], "M": cfg["M"], "N": cfg["N"],
+            "iterations_per_step": cfg["K"], "window": cfg["window"], "S": 3,
+            "parallelism": f"batch-shard x{ngpu} (images split across GPUs, no collective in the loop)",
+            "l2": "inputs larger than L2 (about 44 B/px of state per GPU)"}
+
+
+def main():
+    args = parse()
+    cfg = workload(args)
+    cfg["name"] = args.config
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        out = run_reference(args, cfg, rank)
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return 0
+
+    import numpy as np
+    import torch
+    from paper_2003_12693_b200 import Solver
+    from synth import make_config
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    B = cfg["batch"]
+    assert B % world == 0, "images must divide across ranks"
+    mine = list(range(rank * B // world, (rank + 1) * B // world))
+    if args.config == "c3":
+        data = make_config("c3", images=mine)
+    else:
+        data = make_config(args.config)
+        mine = [0]
+    nb = len(mine)
+    M, N, K = cfg["M"], cfg["N"], cfg["K"]
+    p = data["params"]
+    keys = ("gamma", "alpha", "beta", "mu", "epsilon", "l", "d", "window_shape", "tau", "S", "rho", "sigma",
+            "s", "phi_clip", "w_proj", "w_mode", "w_iters")
+    stream = torch.cuda.Stream(dev)
+    sv = Solver(M, N, nb, window=p["window"], device=local, stream=stream, **{k: p[k] for k in keys})
+    img_d = torch.from_numpy(data["image"]).to(dev)
+    phi0_d = torch.from_numpy(data["phi0"]).to(dev)
+    out_d = torch.empty_like(phi0_d)
+    torch.cuda.synchronize()
+
+    def step_device():
+        sv.set_image(img_d, phi0_d)
+        sv.iterate(K)
+        sv.get_phi(out_d)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---------------------------------------------------------------- device-resident timing (value)
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step_device()
+        sv.sync()
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clk:
+            e0.record(stream)
+            for _ in range(args.steps):
+                step_device()
+            e1.record(stream)
+            torch.cuda.synchronize()
+        sv.sync()
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    ms_step = ms / args.steps
+    px_total = B * M * N
+    value = px_total * K * args.steps / (ms / 1e3) / 1e6
+
+    # ---------------------------------------------------------------- per-kernel roofline (profile pass)
+    sv.set_image(img_d, phi0_d)
+    prof_iters = 2
+    prof = sv.profile(prof_iters)
+    px_rank = nb * M * N
+    dom = max(prof, key=lambda k: prof[k][0])
+    dom_ms, dom_n = prof[dom]
+    peak, peak_src = peaks()
+    achieved = BYTES_PER_PX[dom] * px_rank / (dom_ms / dom_n / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        t = json.load(open(tpath))
+        if t.get("workload") == args.config and dom in t.get("per_launch_bytes", {}):
+            traffic = t["per_launch_bytes"][dom]
+    iter_ms = sum(v[0] for v in prof.values()) / prof_iters
+    kernels = {k: {"ms_per_launch": v[0] / v[1], "launches_per_iter": v[1] // prof_iters,
+                   "share": v[0] / sum(x[0] for x in prof.values()),
+                   "GBs": BYTES_PER_PX[k] * px_rank / (v[0] / v[1] / 1e3) / 1e9} for k, v in prof.items()}
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "bytes_per_px_per_launch": BYTES_PER_PX[dom],
+                "step_model": {"bytes_per_px_iter": MODEL_BYTES_PER_PX_ITER,
+                               "achieved_GBs": MODEL_BYTES_PER_PX_ITER * px_rank * K / (ms_step / 1e3) / 1e9,
+                               "frac": MODEL_BYTES_PER_PX_ITER * px_rank * K / (ms_step / 1e3) / 1e9 / peak},
+                "kernels": kernels, "profiled_iteration_ms": iter_ms}
+
+    # ---------------------------------------------------------------- end to end through host buffers
+    e2e = None
+    if not args.no_e2e:
+        img_h = torch.from_numpy(data["image"]).pin_memory()
+        phi0_h = torch.from_numpy(data["phi0"]).pin_memory()
+        out_h = torch.empty_like(phi0_h).pin_memory()
+
+        def step_host():
+            sv.set_image(img_h, phi0_h)      # H2D inside the call
+            sv.iterate(K)
+            sv.get_phi(out_h)                # D2H inside the call
+        with torch.cuda.stream(stream):
+            step_host()
+            sv.sync()
+            barrier()
+            torch.cuda.synchronize()
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record(stream)
+            for _ in range(args.steps):
+                step_host()
+            f1.record(stream)
+            torch.cuda.synchronize()
+            sv.sync()
+        barrier()
+        ems = max_over_ranks(f0.elapsed_time(f1))
+        e2e = {"value": px_total * K * args.steps / (ems / 1e3) / 1e6, "unit": UNIT,
+               "h2d_bytes_per_step": int(img_h.numel() * 4 + phi0_h.numel() * 4) * world,
+               "d2h_bytes_per_step": int(out_h.numel() * 4) * world, "ms_per_step": ems / args.steps}
+
+    launches = args.steps * (4 + K * sv.launches_per_iteration)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline_oracle(cfg)
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+               "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config_json(cfg, world),
+               "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches * world,
+               "clocks": clk.summary()}
+        print(json.dumps(out), flush=True)
+    sv.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,145 @@
+/*
+ * srsb.h -- C ABI of the B200-native Split Bregman Self-repelling Snake library (libsrsb.so).
+ *
+ * Method: Pan et al., "Using the Split Bregman Algorithm to Solve the
+ * Self-repelling Snake Model", arXiv 2003.12693.  "P:n" is line n of the
+ * paper's LaTeX source; equation numbers are LaTeX's.  Readings
+ * where the paper is silent or garbled are the Q-items of DESIGN.md §2.
+ *
+ * What the library computes: for a batch of B images of
+ * M x N pixels (fp32), Algorithm 1:
+ *   set_image:  g = 1/(1 + rho |grad(G_sigma * f)|^s)              Eq. (1)
+ *               phi = phi0, w = grad phi0, b = 0                    Alg. 1 (1)
+ *   iterate(K): K times { S times { F = Eq. (37) RHS; phi = Re F^-1(F(F)/symbol) Eq. (33) };
+ *                         phi = clamp(phi, -phi_clip, phi_clip)     (north star, Q9)
+ *                         w = proj(shrink(B)) Eq. (41),(42),(40);  b += grad phi - w  Eq. (23) }
+ * All arithmetic runs in hand-written sm_100a CUDA kernels; there is no
+ * CPU fallback.
+ *
+ * Conventions (all calls):
+ *  - Fields are row-major float32: scalar fields [batch][M][N]; vector fields
+ *    (w, b) [batch][2][M][N] with channel 0 the row (i) component and channel
+ *    1 the column (j) component of Eq. (35).  phi < 0 is INSIDE (Eq. 3).
+ *  - Pointers may be device pointers on the context's device OR host
+ *    pointers (pinned or pageable); copies use cudaMemcpyDefault under UVA.
+ *    The caller owns every buffer; the library copies in/out during the call
+ *    and never retains caller pointers.
+ *  - All calls are stream-ordered on the context's stream and asynchronous
+ *    with respect to the host for device pointers; call sr_sb_sync before
+ *    reading outputs.  With pageable host pointers the copy is synchronous.
+ *  - Argument validation is synchronous and happens before any enqueue;
+ *    errors return a negative sr_status and set sr_sb_last_error(ctx).
+ *  - A context is bound to one device and one stream and is not thread-safe.
+ */
+#ifndef SRSB_H
+#define SRSB_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SRSB_ABI_VERSION 1
+
+typedef enum {
+    SR_OK = 0,
+    SR_ERR_ARG = -1,        /* invalid parameter or NULL pointer */
+    SR_ERR_SHAPE = -2,      /* M, N not powers of two in [8, 8192], batch < 1 */
+    SR_ERR_CUDA = -3,       /* CUDA runtime error; message in sr_sb_last_error */
+    SR_ERR_NONFINITE = -5,  /* NaN/Inf or |b| > b_max latched by the w/b kernel */
+    SR_ERR_STATE = -6,      /* call order violated (e.g. iterate before set_image) */
+    SR_ERR_OOM = -7         /* device allocation failed */
+} sr_status;
+
+typedef enum { SR_WIN_DISC = 0, SR_WIN_SQUARE = 1 } sr_window_shape;   /* Q2 */
+typedef enum { SR_WPROJ_BALL = 0, SR_WPROJ_SPHERE = 1, SR_WPROJ_NONE = 2 } sr_wproj;  /* Eq. (40), Q1 */
+typedef enum { SR_W_THRESHOLD = 0, SR_W_FIXED_POINT = 1 } sr_wmode;   /* Eq. (42) / Eq. (39) */
+
+typedef struct {
+    int   M, N, batch;         /* rows, columns (powers of two, 8..8192), images in this context */
+    float gamma, alpha, beta;  /* Eq. (7): geodesic length, balloon, repulsion weights */
+    float mu;                  /* Eq. (22): Bregman penalty */
+    float epsilon;             /* Eq. (5),(6): half-width of the regularized H / delta */
+    float l;                   /* Eq. (11): narrow-band offset of h (the PAPER's l) */
+    float d;                   /* Eq. (10): Gaussian scale exp(-|x-y|^2/d^2) */
+    int   window;              /* summation radius R of the window (BASELINE's "l"), 0..8 */
+    int   window_shape;        /* sr_window_shape: disc p^2+q^2 <= R^2 (default) or square */
+    float tau;                 /* Eq. (30),(37): time step of a phi sweep */
+    int   S;                   /* phi sweeps (FFT solves) per outer iteration, >= 1 (Q7) */
+    float rho, sigma;          /* Eq. (1): edge scale, Gaussian pre-smoothing std (radius ceil(3 sigma) <= 8) */
+    int   s;                   /* Eq. (1): power, 1 or 2 */
+    float phi_clip;            /* > 0: clamp phi^{k+1} to [-phi_clip, phi_clip] after the last sweep; 0: off */
+    int   w_proj;              /* sr_wproj (Q1) */
+    int   w_mode;              /* sr_wmode */
+    int   w_iters;             /* fixed-point sweeps r for SR_W_FIXED_POINT (Eq. 38-39), >= 1 */
+    float b_max;               /* guard: |b| > b_max latches SR_ERR_NONFINITE (SPEC S:366 uses 50); <= 0 off */
+} sr_sb_params;
+
+typedef struct sr_sb_ctx sr_sb_ctx;
+
+/* Fill *p with the defaults of DESIGN.md §2 (Fig. 1 caption P:465 with readings Q17, Q22). */
+void sr_sb_default_params(sr_sb_params* p, int M, int N, int batch, int window);
+
+/* Validate p, allocate all state on `device` (fields, spectrum, tables) and bind
+ * the context to `stream` (a cudaStream_t; NULL = the legacy default stream).
+ * Device memory: about 44 bytes per pixel. */
+sr_status sr_sb_create(const sr_sb_params* p, int device, void* stream, sr_sb_ctx** out);
+
+/* Algorithm 1 step (1): image f and initial level set phi0 ([batch][M][N]) ->
+ * g (Eq. 1), phi = phi0, w = grad phi0 (Q12), b = 0.  Resets k to 0. */
+sr_status sr_sb_set_image(sr_sb_ctx* ctx, const float* image, const float* phi0);
+
+/* Enqueue K outer iterations of Algorithm 1 (each: S sweeps of Eq. 37 + Eq. 33,
+ * the clamp, Eq. 42/40 and Eq. 23).  K >= 0.  Asynchronous. */
+sr_status sr_sb_iterate(sr_sb_ctx* ctx, int K);
+
+/* Copy phi ([batch][M][N]) to phi_out.  Also reports a latched SR_ERR_NONFINITE. */
+sr_status sr_sb_get_phi(sr_sb_ctx* ctx, float* phi_out);
+
+/* Copy the full state; any pointer may be NULL to skip it.  w, b: [batch][2][M][N]. */
+sr_status sr_sb_get_state(sr_sb_ctx* ctx, float* phi, float* w, float* b, float* g);
+
+/* Overwrite the state (checkpoint resume / teacher forcing).  g may be NULL to keep it. */
+sr_status sr_sb_set_state(sr_sb_ctx* ctx, const float* phi, const float* w, const float* b, const float* g);
+
+/* Outer iterations completed since set_image / set_state. */
+long long sr_sb_iteration(const sr_sb_ctx* ctx);
+
+/* Block the host until the context's stream is idle; returns pending CUDA / non-finite errors. */
+sr_status sr_sb_sync(sr_sb_ctx* ctx);
+
+/* Debug / parity entry points (single steps of the hot path, same kernels):
+ *  sr_sb_debug_solve: phi_out = Re F^-1(F(F)/symbol) (Eq. 33) for F [batch][M][N];
+ *                     uses the context's spectrum scratch, leaves the state untouched.
+ *  sr_sb_debug_rhs:   F_out = Eq. (37) RHS evaluated on the current state (psi = phi).
+ *  sr_sb_debug_wb:    one w/b update (Eq. 41/42 or 38/39, 40, 23) on the current state,
+ *                     treating the current phi as phi^{k+1}. */
+sr_status sr_sb_debug_solve(sr_sb_ctx* ctx, const float* F, float* phi_out);
+sr_status sr_sb_debug_rhs(sr_sb_ctx* ctx, float* F_out);
+sr_status sr_sb_debug_wb(sr_sb_ctx* ctx);
+
+/* Kernel classes of the hot path, in launch order within a sweep / iteration. */
+typedef enum { SR_K_RHS = 0, SR_K_ROWS_R2C = 1, SR_K_COLS_SOLVE = 2, SR_K_ROWS_C2R = 3, SR_K_WB = 4,
+               SR_K_NCLASSES = 5 } sr_kernel_class;
+
+/* Diagnostics: run K outer iterations WITHOUT the CUDA graph, bracketing every launch with CUDA
+ * events on the context's work stream, and return per kernel class (sr_kernel_class) the summed
+ * device time in ms (ms_out[5]) and the number of launches (launches_out[5]).  Synchronizes the
+ * host.  Advances the state exactly like sr_sb_iterate(ctx, K). */
+sr_status sr_sb_profile(sr_sb_ctx* ctx, int K, float* ms_out, int* launches_out);
+
+/* Number of kernel launches one outer iteration enqueues (for bench accounting). */
+int sr_sb_launches_per_iteration(const sr_sb_ctx* ctx);
+
+/* Free everything the context owns.  NULL is a no-op. */
+void sr_sb_destroy(sr_sb_ctx* ctx);
+
+/* Message of the last error on ctx (ctx-owned, valid until the next call); ctx may be NULL
+ * for errors of sr_sb_create. */
+const char* sr_sb_last_error(const sr_sb_ctx* ctx);
+
+int sr_sb_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SRSB_H */

@@ -1,0 +1,339 @@
+// sr_fft.cuh -- hand-written power-of-two FFT passes for the phi sub-problem (sm_100a).
+//
+// Solves (1 - tau mu Delta_per) phi = F, i.e. phi = Re F^-1( F(F) / symbol ),
+// Eq. (31)-(33), with the symbol of Eq. (32) read as
+// 1 + tau mu (4 - 2 cos z1 - 2 cos z2) (Q10).  Three HBM passes:
+//
+//   k_rows_r2c   : each image row of N reals -> N/2 + 1 bins (N/2-point complex
+//                  FFT of (x[2n], x[2n+1]) + split), bins 0 and N/2 packed into
+//                  slot 0 (both real); stored TRANSPOSED in column groups:
+//                  spec[b][k2 / G][m][k2 % G]  (complex64)
+//   k_cols_solve : per spectrum column (contiguous M complex): forward M-point FFT,
+//                  multiply by 1 / (M (N/2) symbol(k1, k2)) (the packed slot 0 is
+//                  unpacked to the k2 = 0 and k2 = N/2 symbols), inverse FFT, in place
+//   k_rows_c2r   : transposed load, inverse real FFT, optional clamp, phi rows
+//
+// Inside a CTA each transform is a Stockham autosort FFT: every thread holds
+// E (<= 16) complex values in registers, runs radix-R (R <= 16) butterflies in
+// registers and exchanges through shared memory between stages (one padded
+// SoA row per transform).  Twiddles come from fp32 tables computed in fp64 on
+// the host.  No cuFFT.
+#pragma once
+#include <cuda_runtime.h>
+
+namespace srsb {
+
+__device__ __forceinline__ int pad32(int i) { return i + (i >> 5); }
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ float2 conjf2(float2 a) { return make_float2(a.x, -a.y); }
+
+__host__ __device__ constexpr int brevn(int k, int bits) {
+    int r = 0;
+    for (int i = 0; i < bits; i++) r |= ((k >> i) & 1) << (bits - 1 - i);
+    return r;
+}
+
+// d * exp(-+ 2 pi i idx / 16); idx is a compile-time constant after unrolling.
+template <bool INV>
+__device__ __forceinline__ float2 tw16(float2 d, int idx) {
+    idx &= 15;
+    if (idx == 0) return d;
+    if (idx == 8) return make_float2(-d.x, -d.y);
+    if (idx == 4) return INV ? make_float2(-d.y, d.x) : make_float2(d.y, -d.x);
+    if (idx == 12) return INV ? make_float2(d.y, -d.x) : make_float2(-d.y, d.x);
+    const float C[16] = {1.0f, 0.92387953251128674f, 0.70710678118654752f, 0.38268343236508977f,
+                         0.0f, -0.38268343236508977f, -0.70710678118654752f, -0.92387953251128674f,
+                         -1.0f, -0.92387953251128674f, -0.70710678118654752f, -0.38268343236508977f,
+                         0.0f, 0.38268343236508977f, 0.70710678118654752f, 0.92387953251128674f};
+    const float Sn[16] = {0.0f, 0.38268343236508977f, 0.70710678118654752f, 0.92387953251128674f,
+                          1.0f, 0.92387953251128674f, 0.70710678118654752f, 0.38268343236508977f,
+                          0.0f, -0.38268343236508977f, -0.70710678118654752f, -0.92387953251128674f,
+                          -1.0f, -0.92387953251128674f, -0.70710678118654752f, -0.38268343236508977f};
+    const float c = C[idx], s = INV ? Sn[idx] : -Sn[idx];
+    return make_float2(d.x * c - d.y * s, d.x * s + d.y * c);
+}
+
+// In-register DFT of size R (<= 16): radix-2 decimation in frequency, then bit reversal.
+template <int R, bool INV>
+__device__ __forceinline__ void dft_reg(float2 (&x)[R]) {
+#pragma unroll
+    for (int len = R; len >= 2; len >>= 1) {
+        const int half = len >> 1;
+#pragma unroll
+        for (int s = 0; s < R; s += len) {
+#pragma unroll
+            for (int k = 0; k < half; k++) {
+                const float2 a = x[s + k], b = x[s + k + half];
+                x[s + k] = make_float2(a.x + b.x, a.y + b.y);
+                x[s + k + half] = tw16<INV>(make_float2(a.x - b.x, a.y - b.y), k * (16 / len));
+            }
+        }
+    }
+    constexpr int LOGR = (R >= 16) ? 4 : (R >= 8) ? 3 : (R >= 4) ? 2 : (R >= 2) ? 1 : 0;
+    float2 y[R];
+#pragma unroll
+    for (int k = 0; k < R; k++) y[k] = x[brevn(k, LOGR)];
+#pragma unroll
+    for (int k = 0; k < R; k++) x[k] = y[k];
+}
+
+// Stockham stages of an N-point FFT (N = 2^LOGN) by T = N/E threads, thread t.
+// On entry of the first stage v[u] = x[t + u T]; on exit v[u] = X[t + u T].
+// sre/sim: this transform's padded SoA shared-memory row.  tw[m] = exp(-2 pi i m / N).
+template <int LOGN, int LOGE, int LOGNS, bool INV>
+__device__ __forceinline__ void fft_stages(float2 (&v)[1 << LOGE], float* __restrict__ sre,
+                                           float* __restrict__ sim, int t,
+                                           const float2* __restrict__ tw) {
+    constexpr int N = 1 << LOGN, E = 1 << LOGE, T = N / E;
+    constexpr int LOGR = (LOGN - LOGNS < LOGE) ? (LOGN - LOGNS) : LOGE;
+    constexpr int R = 1 << LOGR, Q = E / R, NS = 1 << LOGNS;
+    constexpr bool LAST = (LOGNS + LOGR == LOGN);
+    if constexpr (LOGNS > 0) {
+#pragma unroll
+        for (int q = 0; q < Q; q++)
+#pragma unroll
+            for (int r = 0; r < R; r++) {
+                const int idx = pad32(t + q * T + r * (N / R));
+                v[q + r * Q] = make_float2(sre[idx], sim[idx]);
+            }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < Q; q++) {
+        const int j = t + q * T;
+        const int k = j & (NS - 1);
+        float2 x[R];
+#pragma unroll
+        for (int r = 0; r < R; r++) x[r] = v[q + r * Q];
+        if constexpr (LOGNS > 0) {
+            constexpr int STRIDE = N / (NS * R);
+            float2 pw[LOGR];
+#pragma unroll
+            for (int bb = 0; bb < LOGR; bb++) {
+                const float2 w = __ldg(&tw[(k * STRIDE) << bb]);
+                pw[bb] = INV ? conjf2(w) : w;
+            }
+#pragma unroll
+            for (int r = 1; r < R; r++) {
+                float2 w = make_float2(1.f, 0.f);
+                bool first = true;
+#pragma unroll
+                for (int bb = 0; bb < LOGR; bb++)
+                    if ((r >> bb) & 1) {
+                        w = first ? pw[bb] : cmul(w, pw[bb]);
+                        first = false;
+                    }
+                x[r] = cmul(x[r], w);
+            }
+        }
+        dft_reg<R, INV>(x);
+        if constexpr (LAST) {
+#pragma unroll
+            for (int r = 0; r < R; r++) v[q + r * Q] = x[r];
+        } else {
+            const int base = (j >> LOGNS) * (NS * R) + k;
+#pragma unroll
+            for (int r = 0; r < R; r++) {
+                const int idx = pad32(base + r * NS);
+                sre[idx] = x[r].x;
+                sim[idx] = x[r].y;
+            }
+        }
+    }
+    if constexpr (!LAST) {
+        __syncthreads();
+        fft_stages<LOGN, LOGE, LOGNS + LOGR, INV>(v, sre, sim, t, tw);
+    }
+}
+
+struct FftRowArgs {
+    int M;          // rows per image
+    int lg_rpc;     // log2 rows per CTA
+    int lg_G;       // log2 column-group interleave of the spectrum
+    int SR;         // floats per shared row (re or im), padded
+    float clip;     // c2r only: > 0 clamps the output to [-clip, clip]
+};
+
+// Row pass 1: F rows (N = 2H reals) -> transposed packed half spectrum.
+template <int LOGH, int LOGE>
+__global__ void __launch_bounds__(512) k_rows_r2c(const float* __restrict__ F, float2* __restrict__ spec,
+                                                   const float2* __restrict__ twH,
+                                                   const float2* __restrict__ twR, FftRowArgs a) {
+    constexpr int H = 1 << LOGH, E = 1 << LOGE, T = H / E;
+    extern __shared__ float smem[];
+    const int tid = threadIdx.x;
+    const int grp = tid / T, t = tid % T;
+    const int rpc = 1 << a.lg_rpc, G = 1 << a.lg_G;
+    const int b = blockIdx.y, m0 = blockIdx.x * rpc;
+    float* sre = smem + grp * 2 * a.SR;
+    float* sim = sre + a.SR;
+    const float2* x = reinterpret_cast<const float2*>(F + ((size_t)b * a.M + m0 + grp) * (2 * H));
+    float2 v[E];
+#pragma unroll
+    for (int u = 0; u < E; u++) v[u] = __ldcs(x + t + u * T);
+    fft_stages<LOGH, LOGE, 0, false>(v, sre, sim, t, twH);
+#pragma unroll
+    for (int u = 0; u < E; u++) {
+        const int idx = pad32(t + u * T);
+        sre[idx] = v[u].x;
+        sim[idx] = v[u].y;
+    }
+    __syncthreads();
+    const int total = rpc * H;
+    float2* out = spec + (size_t)b * H * a.M;
+    for (int e = tid; e < total; e += blockDim.x) {
+        const int kk = e & (G - 1);
+        const int rr = (e >> a.lg_G) & (rpc - 1);
+        const int kg = e >> (a.lg_G + a.lg_rpc);
+        const int k2 = (kg << a.lg_G) + kk;
+        const float* rre = smem + rr * 2 * a.SR;
+        const float* rim = rre + a.SR;
+        const float2 Zk = make_float2(rre[pad32(k2)], rim[pad32(k2)]);
+        const int kc = (H - k2) & (H - 1);
+        const float2 Zc = make_float2(rre[pad32(kc)], -rim[pad32(kc)]);
+        float2 X;
+        if (k2 == 0) {
+            X = make_float2(Zk.x + Zk.y, Zk.x - Zk.y);  // (X[0], X[N/2]) packed
+        } else {
+            const float2 Ev = make_float2(0.5f * (Zk.x + Zc.x), 0.5f * (Zk.y + Zc.y));
+            const float2 D = make_float2(0.5f * (Zk.x - Zc.x), 0.5f * (Zk.y - Zc.y));
+            const float2 O = make_float2(D.y, -D.x);  // -i D
+            const float2 wo = cmul(__ldg(&twR[k2]), O);
+            X = make_float2(Ev.x + wo.x, Ev.y + wo.y);
+        }
+        out[(((size_t)kg * a.M + m0 + rr) << a.lg_G) + kk] = X;
+    }
+}
+
+struct FftColArgs {
+    int H;          // N/2: spectrum columns
+    int lg_G;       // columns per CTA (= layout interleave)
+    int SC;         // floats per shared row, padded
+    float taumu;    // tau * mu
+    float scale;    // 1 / (M H)
+};
+
+// Column pass: forward FFT, divide by the symbol, inverse FFT, in place.
+template <int LOGM, int LOGE>
+__global__ void __launch_bounds__(512) k_cols_solve(float2* __restrict__ spec, const float2* __restrict__ twM,
+                                                     const float* __restrict__ cM, const float* __restrict__ cN,
+                                                     FftColArgs a) {
+    constexpr int M = 1 << LOGM, E = 1 << LOGE, T = M / E;
+    extern __shared__ float smem[];
+    const int G = 1 << a.lg_G;
+    const int tid = threadIdx.x;
+    const int cc = tid & (G - 1), t = tid >> a.lg_G;
+    const int kg = blockIdx.x, b = blockIdx.y;
+    const int k2 = (kg << a.lg_G) + cc;
+    float2* base = spec + (size_t)b * a.H * M + (size_t)kg * M * G;
+    float* sre = smem + cc * 2 * a.SC;
+    float* sim = sre + a.SC;
+    float2 v[E];
+#pragma unroll
+    for (int u = 0; u < E; u++) v[u] = base[((t + u * T) << a.lg_G) + cc];
+    fft_stages<LOGM, LOGE, 0, false>(v, sre, sim, t, twM);
+    if (kg == 0) {  // CTA-uniform branch: slot 0 packs the real columns k2 = 0 and k2 = N/2
+#pragma unroll
+        for (int u = 0; u < E; u++) {
+            const int idx = pad32(t + u * T);
+            sre[idx] = v[u].x;
+            sim[idx] = v[u].y;
+        }
+        __syncthreads();
+        if (cc == 0) {
+            const float c0 = __ldg(&cN[0]), ch = __ldg(&cN[a.H]);
+#pragma unroll
+            for (int u = 0; u < E; u++) {
+                const int k1 = t + u * T;
+                const int kc = (M - k1) & (M - 1);
+                const float2 C = v[u];
+                const float2 Cc = make_float2(sre[pad32(kc)], -sim[pad32(kc)]);
+                const float cm = __ldg(&cM[k1]);
+                const float s0 = a.scale / (1.f + a.taumu * (cm + c0));
+                const float sh = a.scale / (1.f + a.taumu * (cm + ch));
+                const float p = 0.5f * (s0 + sh), m = 0.5f * (s0 - sh);
+                v[u] = make_float2(p * C.x + m * Cc.x, p * C.y + m * Cc.y);
+            }
+        } else {
+            const float ck = __ldg(&cN[k2]);
+#pragma unroll
+            for (int u = 0; u < E; u++) {
+                const float s = a.scale / (1.f + a.taumu * (__ldg(&cM[t + u * T]) + ck));
+                v[u] = make_float2(v[u].x * s, v[u].y * s);
+            }
+        }
+        __syncthreads();
+    } else {
+        const float ck = __ldg(&cN[k2]);
+#pragma unroll
+        for (int u = 0; u < E; u++) {
+            const float s = a.scale / (1.f + a.taumu * (__ldg(&cM[t + u * T]) + ck));
+            v[u] = make_float2(v[u].x * s, v[u].y * s);
+        }
+    }
+    fft_stages<LOGM, LOGE, 0, true>(v, sre, sim, t, twM);
+#pragma unroll
+    for (int u = 0; u < E; u++) base[((t + u * T) << a.lg_G) + cc] = v[u];
+}
+
+// Row pass 2: transposed half spectrum -> inverse real FFT -> phi rows (optionally clamped).
+template <int LOGH, int LOGE>
+__global__ void __launch_bounds__(512) k_rows_c2r(const float2* __restrict__ spec, float* __restrict__ phi,
+                                                   const float2* __restrict__ twH,
+                                                   const float2* __restrict__ twR, FftRowArgs a) {
+    constexpr int H = 1 << LOGH, E = 1 << LOGE, T = H / E;
+    extern __shared__ float smem[];
+    const int tid = threadIdx.x;
+    const int grp = tid / T, t = tid % T;
+    const int rpc = 1 << a.lg_rpc, G = 1 << a.lg_G;
+    const int b = blockIdx.y, m0 = blockIdx.x * rpc;
+    const float2* in = spec + (size_t)b * H * a.M;
+    const int total = rpc * H;
+    for (int e = tid; e < total; e += blockDim.x) {
+        const int kk = e & (G - 1);
+        const int rr = (e >> a.lg_G) & (rpc - 1);
+        const int kg = e >> (a.lg_G + a.lg_rpc);
+        const int k2 = (kg << a.lg_G) + kk;
+        const float2 X = in[(((size_t)kg * a.M + m0 + rr) << a.lg_G) + kk];
+        float* rre = smem + rr * 2 * a.SR;
+        rre[pad32(k2)] = X.x;
+        rre[a.SR + pad32(k2)] = X.y;
+    }
+    __syncthreads();
+    float* sre = smem + grp * 2 * a.SR;
+    float* sim = sre + a.SR;
+    float2 v[E];
+#pragma unroll
+    for (int u = 0; u < E; u++) {
+        const int k = t + u * T;
+        const float2 X = make_float2(sre[pad32(k)], sim[pad32(k)]);
+        if (k == 0) {
+            // X.x = X[0], X.y = X[N/2]: Z[0] = E[0] + i O[0], E = (X0 + Xh)/2, O = (X0 - Xh)/2
+            v[u] = make_float2(0.5f * (X.x + X.y), 0.5f * (X.x - X.y));
+        } else {
+            const int kc = H - k;
+            const float2 Xc = make_float2(sre[pad32(kc)], -sim[pad32(kc)]);
+            const float2 Ev = make_float2(0.5f * (X.x + Xc.x), 0.5f * (X.y + Xc.y));
+            const float2 D = make_float2(0.5f * (X.x - Xc.x), 0.5f * (X.y - Xc.y));
+            const float2 O = cmul(conjf2(__ldg(&twR[k])), D);  // W^{-k} D
+            v[u] = make_float2(Ev.x - O.y, Ev.y + O.x);        // E + i O
+        }
+    }
+    __syncthreads();
+    fft_stages<LOGH, LOGE, 0, true>(v, sre, sim, t, twH);
+    float2* out = reinterpret_cast<float2*>(phi + ((size_t)b * a.M + m0 + grp) * (2 * H));
+#pragma unroll
+    for (int u = 0; u < E; u++) {
+        float2 z = v[u];
+        if (a.clip > 0.f) {
+            z.x = fminf(fmaxf(z.x, -a.clip), a.clip);
+            z.y = fminf(fmaxf(z.y, -a.clip), a.clip);
+        }
+        out[t + u * T] = z;
+    }
+}
+
+}  // namespace srsb

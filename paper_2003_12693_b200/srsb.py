@@ -1,0 +1,212 @@
+"""Thin ctypes binding of libsrsb.so (include/srsb.h).  Argument marshalling only: every step
+of the Split Bregman SR iteration runs in the library's CUDA kernels.  There is no CPU
+fallback: if the library is missing or no GPU is present, construction raises.
+
+Names follow the C ABI: sr_sb_create -> Solver(...), sr_sb_set_image -> Solver.set_image,
+sr_sb_iterate -> Solver.iterate, sr_sb_get_phi -> Solver.get_phi.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsrsb.so")
+
+SR_OK, SR_ERR_ARG, SR_ERR_SHAPE, SR_ERR_CUDA, SR_ERR_NONFINITE, SR_ERR_STATE, SR_ERR_OOM = 0, -1, -2, -3, -5, -6, -7
+STATUS_NAMES = {0: "SR_OK", -1: "SR_ERR_ARG", -2: "SR_ERR_SHAPE", -3: "SR_ERR_CUDA", -5: "SR_ERR_NONFINITE",
+                -6: "SR_ERR_STATE", -7: "SR_ERR_OOM"}
+
+# every symbol include/srsb.h declares (checked by tests/test_abi.py)
+EXPORTS = ["sr_sb_default_params", "sr_sb_create", "sr_sb_set_image", "sr_sb_iterate", "sr_sb_get_phi",
+           "sr_sb_get_state", "sr_sb_set_state", "sr_sb_iteration", "sr_sb_sync", "sr_sb_debug_solve",
+           "sr_sb_debug_rhs", "sr_sb_debug_wb", "sr_sb_launches_per_iteration", "sr_sb_destroy",
+           "sr_sb_last_error", "sr_sb_abi_version", "sr_sb_profile"]
+KERNEL_CLASSES = ["rhs", "rows_r2c", "cols_solve", "rows_c2r", "wb"]
+
+
+class SrsbError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Params(C.Structure):
+    """Mirror of sr_sb_params (include/srsb.h)."""
+    _fields_ = [("M", C.c_int), ("N", C.c_int), ("batch", C.c_int),
+                ("gamma", C.c_float), ("alpha", C.c_float), ("beta", C.c_float), ("mu", C.c_float),
+                ("epsilon", C.c_float), ("l", C.c_float), ("d", C.c_float), ("window", C.c_int),
+                ("window_shape", C.c_int), ("tau", C.c_float), ("S", C.c_int), ("rho", C.c_float),
+                ("sigma", C.c_float), ("s", C.c_int), ("phi_clip", C.c_float), ("w_proj", C.c_int),
+                ("w_mode", C.c_int), ("w_iters", C.c_int), ("b_max", C.c_float)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libsrsb.so (raises if it has not been built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built; run `python -m paper_2003_12693_b200.build`")
+        L = C.CDLL(LIB_PATH)
+        p, i, st = C.c_void_p, C.c_int, C.c_int
+        sig = {
+            "sr_sb_default_params": (None, [C.POINTER(Params), i, i, i, i]),
+            "sr_sb_create": (st, [C.POINTER(Params), i, p, C.POINTER(p)]),
+            "sr_sb_set_image": (st, [p, p, p]),
+            "sr_sb_iterate": (st, [p, i]),
+            "sr_sb_get_phi": (st, [p, p]),
+            "sr_sb_get_state": (st, [p, p, p, p, p]),
+            "sr_sb_set_state": (st, [p, p, p, p, p]),
+            "sr_sb_iteration": (C.c_longlong, [p]),
+            "sr_sb_sync": (st, [p]),
+            "sr_sb_debug_solve": (st, [p, p, p]),
+            "sr_sb_debug_rhs": (st, [p, p]),
+            "sr_sb_debug_wb": (st, [p]),
+            "sr_sb_launches_per_iteration": (i, [p]),
+            "sr_sb_destroy": (None, [p]),
+            "sr_sb_last_error": (C.c_char_p, [p]),
+            "sr_sb_abi_version": (i, []),
+            "sr_sb_profile": (st, [p, i, C.POINTER(C.c_float), C.POINTER(C.c_int)]),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def default_params(M, N, batch=1, window=4) -> dict:
+    p = Params()
+    lib().sr_sb_default_params(C.byref(p), M, N, batch, window)
+    return {name: getattr(p, name) for name, _ in Params._fields_}
+
+
+def _ptr(x):
+    """Raw pointer of a contiguous float32 torch tensor (device or host) or numpy array (host)."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        if x.dtype != np.float32 or not x.flags["C_CONTIGUOUS"]:
+            raise ValueError("numpy arrays must be C-contiguous float32")
+        return x.ctypes.data
+    import torch
+    if isinstance(x, torch.Tensor):
+        if x.dtype != torch.float32 or not x.is_contiguous():
+            raise ValueError("tensors must be contiguous float32")
+        return x.data_ptr()
+    raise TypeError(f"unsupported buffer type {type(x)}")
+
+
+class Solver:
+    """One sr_sb context: `batch` images of M x N on one device, bound to one CUDA stream.
+
+    params: any field of sr_sb_params (paper notation); unspecified fields take the
+    library defaults (sr_sb_default_params: DESIGN.md §2).
+    """
+
+    def __init__(self, M, N, batch=1, window=4, device=None, stream=None, **params):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("srsb needs a CUDA device (no CPU fallback)")
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        self.stream = stream
+        p = Params()
+        lib().sr_sb_default_params(C.byref(p), M, N, batch, window)   # d = window (reading Q2)
+        for k, v in params.items():
+            if not hasattr(p, k):
+                raise KeyError(f"unknown parameter {k}")
+            setattr(p, k, v)
+        self.params = {name: getattr(p, name) for name, _ in Params._fields_}
+        self.M, self.N, self.batch = M, N, batch
+        ctx = C.c_void_p()
+        st = lib().sr_sb_create(C.byref(p), self.device.index, C.c_void_p(stream.cuda_stream), C.byref(ctx))
+        if st != SR_OK:
+            raise SrsbError(st, lib().sr_sb_last_error(None).decode())
+        self._ctx = ctx
+
+    # -- plumbing
+    def _check(self, st):
+        if st != SR_OK:
+            raise SrsbError(st, lib().sr_sb_last_error(self._ctx).decode())
+
+    def _field(self, nch=1):
+        import torch
+        return torch.empty((self.batch, nch, self.M, self.N) if nch > 1 else (self.batch, self.M, self.N),
+                           dtype=torch.float32, device=self.device)
+
+    def close(self):
+        if getattr(self, "_ctx", None):
+            lib().sr_sb_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- the four calls of the boundary
+    def set_image(self, image, phi0):
+        self._check(lib().sr_sb_set_image(self._ctx, _ptr(image), _ptr(phi0)))
+
+    def iterate(self, K):
+        self._check(lib().sr_sb_iterate(self._ctx, int(K)))
+
+    def get_phi(self, out=None):
+        out = self._field() if out is None else out
+        self._check(lib().sr_sb_get_phi(self._ctx, _ptr(out)))
+        return out
+
+    # -- extensions
+    def get_state(self):
+        phi, w, b, g = self._field(), self._field(2), self._field(2), self._field()
+        self._check(lib().sr_sb_get_state(self._ctx, _ptr(phi), _ptr(w), _ptr(b), _ptr(g)))
+        return dict(phi=phi, w=w, b=b, g=g)
+
+    def set_state(self, phi, w, b, g=None):
+        self._check(lib().sr_sb_set_state(self._ctx, _ptr(phi), _ptr(w), _ptr(b), _ptr(g)))
+
+    def sync(self):
+        self._check(lib().sr_sb_sync(self._ctx))
+
+    @property
+    def iteration(self):
+        return int(lib().sr_sb_iteration(self._ctx))
+
+    @property
+    def launches_per_iteration(self):
+        return int(lib().sr_sb_launches_per_iteration(self._ctx))
+
+    def profile(self, K):
+        """sr_sb_profile: per kernel class {name: (ms_total, launches)} over K ungraphed iterations."""
+        ms = (C.c_float * 5)()
+        n = (C.c_int * 5)()
+        self._check(lib().sr_sb_profile(self._ctx, int(K), ms, n))
+        return {name: (float(ms[i]), int(n[i])) for i, name in enumerate(KERNEL_CLASSES)}
+
+    def debug_solve(self, F):
+        out = self._field()
+        self._check(lib().sr_sb_debug_solve(self._ctx, _ptr(F), _ptr(out)))
+        return out
+
+    def debug_rhs(self):
+        out = self._field()
+        self._check(lib().sr_sb_debug_rhs(self._ctx, _ptr(out)))
+        return out
+
+    def debug_wb(self):
+        self._check(lib().sr_sb_debug_wb(self._ctx))

@@ -1,0 +1,257 @@
+"""GPU parity: every kernel of the hot path, through the C ABI, against the float64 oracle on the
+same seeded inputs (DESIGN.md §6 for the tolerances and where they come from).
+
+Kernel-level (teacher-forced) checks compare each step on random states that span several
+tiles and a ragged tail; the trajectory checks run Algorithm 1 free for 10 iterations on the
+BASELINE configs (tolerance 1e-4 from north_star) and to completion on C1 (masks).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_2003_12693_b200 import build
+    build.build()
+    from paper_2003_12693_b200 import srsb
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return srsb
+
+
+def _params(window, **over):
+    from synth import paper_params
+    p = paper_params(window)
+    p.update(over)
+    return p
+
+
+def _solver(S, M, N, batch, p):
+    keys = ("gamma", "alpha", "beta", "mu", "epsilon", "l", "d", "window_shape", "tau", "S", "rho", "sigma",
+            "s", "phi_clip", "w_proj", "w_mode", "w_iters")
+    return S.Solver(M, N, batch, window=p["window"], **{k: p[k] for k in keys})
+
+
+def _cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+def _np(t):
+    torch.cuda.synchronize()
+    return t.detach().cpu().numpy().astype(np.float64)
+
+
+def _periodic_residual(phi, F, tau, mu):
+    lap = (np.roll(phi, 1, 0) + np.roll(phi, -1, 0) + np.roll(phi, 1, 1) + np.roll(phi, -1, 1) - 4 * phi)
+    return np.linalg.norm(phi - tau * mu * lap - F) / np.linalg.norm(F)
+
+
+# ----------------------------------------------------------------------------- FFT solve, Eq. (33)
+@pytest.mark.parametrize("M,N,batch", [(8, 8, 1), (16, 64, 2), (64, 16, 1), (128, 128, 1), (32, 512, 1),
+                                       (512, 32, 1), (256, 256, 3), (1024, 1024, 2), (2048, 256, 1),
+                                       (256, 4096, 1), (8192, 16, 1), (16, 8192, 1)])
+def test_solve_parity(S, orc, M, N, batch):
+    p = _params(3)
+    rng = np.random.default_rng(M * 7 + N)
+    F = rng.standard_normal((batch, M, N)).astype(np.float32)
+    with _solver(S, M, N, batch, p) as sv:
+        out = _np(sv.debug_solve(_cuda(F)))
+    for b in range(batch):
+        ref = orc.solve(F[b], p["tau"], p["mu"])
+        err = np.max(np.abs(out[b] - ref))
+        assert err <= 1e-5 * np.max(np.abs(F[b])), (b, err)
+        assert _periodic_residual(out[b], F[b].astype(np.float64), p["tau"], p["mu"]) < 2e-6
+
+
+def test_solve_closed_forms(S):
+    """Constant -> same constant; a single cos mode (k1, k2), including the packed k2 = 0 and
+    k2 = N/2 columns, -> scaled by 1/symbol (Eq. 32)."""
+    M, N, tau, mu = 64, 128, 0.1, 8.0
+    ii, jj = np.meshgrid(np.arange(M), np.arange(N), indexing="ij")
+    modes = [(0, 0), (1, 0), (0, N // 2), (M // 2, N // 2), (5, 0), (7, N // 2), (3, 17), (M - 1, 1)]
+    F = np.stack([np.cos(2 * np.pi * (k1 * ii / M + k2 * jj / N)) for k1, k2 in modes]).astype(np.float32)
+    with _solver(S, M, N, len(modes), _params(3)) as sv:
+        out = _np(sv.debug_solve(_cuda(F)))
+    for b, (k1, k2) in enumerate(modes):
+        sig = 1 + tau * mu * (4 - 2 * np.cos(2 * np.pi * k1 / M) - 2 * np.cos(2 * np.pi * k2 / N))
+        assert np.max(np.abs(out[b] - F[b] / sig)) < 2e-6, (k1, k2)
+
+
+# ----------------------------------------------------------------------------- edge indicator, init
+@pytest.mark.parametrize("M,N", [(128, 128), (8, 64), (256, 512)])
+def test_edge_and_init_parity(S, orc, M, N):
+    from synth import random_state
+    st = random_state(M, N, batch=2, seed=3)
+    p = _params(4)
+    with _solver(S, M, N, 2, p) as sv:
+        sv.set_image(_cuda(st["image"]), _cuda(st["phi"]))
+        s = sv.get_state()
+        g, w, b, phi = _np(s["g"]), _np(s["w"]), _np(s["b"]), _np(s["phi"])
+    for k in range(2):
+        gref = orc.edge(st["image"][k], p["sigma"], p["rho"], p["s"])
+        assert np.max(np.abs(g[k] - gref)) < 2e-6
+        g1, g2 = orc.grad(st["phi"][k])
+        assert np.max(np.abs(w[k, 0] - g1)) < 1e-6 and np.max(np.abs(w[k, 1] - g2)) < 1e-6
+        assert not b[k].any()
+        assert np.array_equal(phi[k], st["phi"][k])
+
+
+# ----------------------------------------------------------------------------- RHS, Eq. (37)
+@pytest.mark.parametrize("M,N,window,shape", [(64, 64, 3, 0), (128, 256, 4, 0), (128, 512, 6, 0), (8, 16, 4, 0),
+                                              (16, 1024, 5, 1), (256, 128, 8, 0), (32, 32, 0, 0), (128, 128, 2, 1)])
+def test_rhs_parity(S, orc, M, N, window, shape):
+    from synth import random_state
+    st = random_state(M, N, batch=2, seed=window)
+    p = _params(window, window_shape=shape, d=max(window, 1) * 0.9)
+    with _solver(S, M, N, 2, p) as sv:
+        w = np.stack([st["w1"], st["w2"]], 1)
+        b = np.stack([st["b1"], st["b2"]], 1)
+        sv.set_state(_cuda(st["phi"]), _cuda(w), _cuda(b), _cuda(st["g"]))
+        F = _np(sv.debug_rhs())
+    for k in range(2):
+        ref = orc.rhs(p, st["phi"][k], st["w1"][k], st["w2"][k], st["b1"][k], st["b2"][k], st["g"][k])
+        err = np.abs(F[k] - ref) / (1 + np.abs(ref))
+        assert err.max() < 2e-5, (k, err.max(), np.unravel_index(err.argmax(), err.shape))
+
+
+# ----------------------------------------------------------------------------- w/b update, Eq. (41),(42),(40),(23)
+@pytest.mark.parametrize("window,proj,mode,iters", [(3, 0, 0, 1), (4, 2, 0, 1), (6, 0, 0, 1), (4, 0, 1, 1),
+                                                    (3, 2, 1, 3)])
+def test_wb_parity(S, orc, window, proj, mode, iters):
+    from synth import random_state
+    M, N = 64, 256
+    st = random_state(M, N, batch=2, seed=10 + window)
+    p = _params(window, w_proj=proj, w_mode=mode, w_iters=iters)
+    with _solver(S, M, N, 2, p) as sv:
+        w = np.stack([st["w1"], st["w2"]], 1)
+        b = np.stack([st["b1"], st["b2"]], 1)
+        sv.set_state(_cuda(st["phi"]), _cuda(w), _cuda(b), _cuda(st["g"]))
+        sv.debug_wb()
+        s = sv.get_state()
+        wg, bg = _np(s["w"]), _np(s["b"])
+    for k in range(2):
+        r1, r2, rb1, rb2 = orc.wb(p, st["phi"][k], st["w1"][k], st["w2"][k], st["b1"][k], st["b2"][k], st["g"][k])
+        for a, r in ((wg[k, 0], r1), (wg[k, 1], r2), (bg[k, 0], rb1), (bg[k, 1], rb2)):
+            assert np.max(np.abs(a - r)) < 2e-5
+
+
+# ----------------------------------------------------------------------------- free-running trajectories
+def _trajectory(S, orc, cfg, K=10, tol=1e-4, check_every=1):
+    p = cfg["params"]
+    B, M, N = cfg["image"].shape
+    errs = []
+    with _solver(S, M, N, B, p) as sv:
+        sv.set_image(_cuda(cfg["image"]), _cuda(cfg["phi0"]))
+        ref = []
+        for b in range(B):
+            g = orc.edge(cfg["image"][b], p["sigma"], p["rho"], p["s"])
+            ref.append((orc.init(cfg["phi0"][b]), g))
+        for k in range(0, K, check_every):
+            sv.iterate(check_every)
+            phi = _np(sv.get_phi())
+            e = 0.0
+            for b in range(B):
+                st, g = ref[b]
+                orc.iterate(p, st, g, check_every)
+                e = max(e, float(np.max(np.abs(phi[b] - st["phi"]))))
+            errs.append(e)
+        sv.sync()
+    assert max(errs) <= tol, errs
+    return errs
+
+
+def test_trajectory_c1(S, orc):
+    from synth import make_config
+    _trajectory(S, orc, make_config("c1"))
+
+
+def test_trajectory_c2(S, orc):
+    from synth import make_config
+    _trajectory(S, orc, make_config("c2"))
+
+
+def test_trajectory_c3_images(S, orc):
+    from synth import make_config
+    _trajectory(S, orc, make_config("c3", images=[0, 1, 2]), K=10, check_every=2)
+
+
+def test_trajectory_c4_small(S, orc):
+    """C4's recipe (thin close curves, R = 6, thresholded init) at 512^2."""
+    from synth import make_config
+    _trajectory(S, orc, make_config("c4", size=(512, 512)))
+
+
+def test_trajectory_c5_small(S, orc):
+    from synth import make_config
+    _trajectory(S, orc, make_config("c5", size=(512, 1024)), K=10, check_every=5)
+
+
+def test_c1_final_masks_and_topology(S, orc):
+    """BASELINE configs[0]: full K = 300; masks {phi < 0} agree on >= 99.9 % of pixels with an
+    identical component count, and that count is 1."""
+    from synth import make_config
+    cfg = make_config("c1")
+    p = cfg["params"]
+    with _solver(S, 128, 128, 1, p) as sv:
+        sv.set_image(_cuda(cfg["image"]), _cuda(cfg["phi0"]))
+        sv.iterate(cfg["K"])
+        phi = _np(sv.get_phi())[0]
+        sv.sync()
+    st = orc.run(p, cfg["image"][0], cfg["phi0"][0], cfg["K"])
+    mg, mo = phi < 0, st["phi"] < 0
+    assert (mg == mo).mean() >= 0.999
+    assert orc.label(mg)[0] == orc.label(mo)[0] == 1
+    assert np.all(np.abs(phi) <= 1.0)
+
+
+def test_iterate_chunking_and_determinism(S):
+    """iterate(7) == iterate(3) + iterate(4) (graph vs direct launches) bitwise; runs are deterministic."""
+    from synth import make_config
+    cfg = make_config("c1")
+    outs = []
+    for chunks in ((7,), (3, 4), (1, 1, 5)):
+        with _solver(S, 128, 128, 1, cfg["params"]) as sv:
+            sv.set_image(_cuda(cfg["image"]), _cuda(cfg["phi0"]))
+            for c in chunks:
+                sv.iterate(c)
+            s = sv.get_state()
+            outs.append({k: _np(v) for k, v in s.items()})
+            assert sv.iteration == 7
+    for o in outs[1:]:
+        for k in o:
+            assert np.array_equal(o[k], outs[0][k]), k
+
+
+def test_host_buffers_and_errors(S):
+    """Host (numpy) pointers work through the same calls; call-order errors are reported."""
+    from synth import make_config
+    cfg = make_config("c1")
+    with _solver(S, 128, 128, 1, cfg["params"]) as sv:
+        with pytest.raises(S.SrsbError):
+            sv.iterate(1)                      # before set_image: SR_ERR_STATE
+        sv.set_image(cfg["image"], cfg["phi0"])
+        sv.iterate(2)
+        host = np.empty((1, 128, 128), np.float32)
+        sv.get_phi(host)
+        sv.sync()
+        dev = _np(sv.get_phi())
+        assert np.array_equal(host.astype(np.float64), dev)
+
+
+def test_nonfinite_guard(S):
+    from synth import make_config
+    cfg = make_config("c1")
+    img = cfg["image"].copy()
+    with _solver(S, 128, 128, 1, cfg["params"]) as sv:
+        sv.set_image(img, cfg["phi0"])
+        st = sv.get_state()
+        b = st["b"].clone()
+        b[0, 0, 5, 5] = float("nan")
+        sv.set_state(st["phi"], st["w"], b)
+        sv.iterate(1)
+        with pytest.raises(S.SrsbError) as ei:
+            sv.sync()
+        assert ei.value.status == S.SR_ERR_NONFINITE

@@ -110,7 +110,9 @@ sr_status sr_sb_sync(sr_sb_ctx* ctx);
 /* Debug / parity entry points (single steps of the hot path, same kernels):
  *  sr_sb_debug_solve: phi_out = Re F^-1(F(F)/symbol) (Eq. 33) for F [batch][M][N];
  *                     uses the context's spectrum scratch, leaves the state untouched.
- *  sr_sb_debug_rhs:   F_out = Eq. (37) RHS evaluated on the current state (psi = phi).
+ *  sr_sb_debug_rhs:   D_out = F - (1 - tau mu Delta_per) psi: the Eq. (37) RHS F in the increment
+ *                     form the solve consumes, evaluated on the current state
+ *                     (psi = phi); Delta_per is the periodic 5-point Laplacian of Eq. (35).
  *  sr_sb_debug_wb:    one w/b update (Eq. 41/42 or 38/39, 40, 23) on the current state,
  *                     treating the current phi as phi^{k+1}. */
 sr_status sr_sb_debug_solve(sr_sb_ctx* ctx, const float* F, float* phi_out);

@@ -155,6 +155,7 @@ struct FftRowArgs {
     int lg_G;       // log2 column-group interleave of the spectrum
     int SR;         // floats per shared row (re or im), padded
     float clip;     // c2r only: > 0 clamps the output to [-clip, clip]
+    int accum;      // c2r only: 1 -> phi = phi + z (increment form), 0 -> phi = z
 };
 
 // Row pass 1: F rows (N = 2H reals) -> transposed packed half spectrum.
@@ -328,6 +329,11 @@ __global__ void __launch_bounds__(512) k_rows_c2r(const float2* __restrict__ spe
 #pragma unroll
     for (int u = 0; u < E; u++) {
         float2 z = v[u];
+        if (a.accum) {
+            const float2 old = out[t + u * T];
+            z.x += old.x;
+            z.y += old.y;
+        }
         if (a.clip > 0.f) {
             z.x = fminf(fmaxf(z.x, -a.clip), a.clip);
             z.y = fminf(fmaxf(z.y, -a.clip), a.clip);

@@ -21,29 +21,90 @@ namespace srsb {
 
 constexpr float kPi = 3.14159265358979323846f;
 
-struct Reg {  // regularizer constants (Eq. 5, 6, 11, 28, 29)
+// ------------------------------------------------------------------ packed f32x2 arithmetic (FFMA2/FADD2)
+__device__ __forceinline__ unsigned long long f2u(float2 a) { return *reinterpret_cast<unsigned long long*>(&a); }
+__device__ __forceinline__ float2 u2f(unsigned long long a) { return *reinterpret_cast<float2*>(&a); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+    unsigned long long d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(c)));
+    return u2f(d);
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+    unsigned long long d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
+    return u2f(d);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+    unsigned long long d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
+    return u2f(d);
+}
+
+// ------------------------------------------------------------------ regularizers (Eq. 5, 6, 11, 28, 29)
+// All of H(x +- l), delta(x +- l), delta(x), delta'(x) from ONE sincospif(x / eps): the arguments
+// (x +- l)/eps differ by the constant l/eps, so sin/cos follow by angle addition with
+// (sinpi(l/eps), cospi(l/eps)) precomputed in double on the host.  Branch conditions use x +- l.
+struct Reg {
     float eps, inv_eps, l;
+    float sl, cl;          // sinpi(l / eps), cospi(l / eps)
 };
 
-__device__ __forceinline__ float Heps(float x, const Reg& r) {
-    if (x > r.eps) return 1.f;
-    if (x < -r.eps) return 0.f;
-    const float a = x * r.inv_eps;
-    return 0.5f * (1.f + a + sinpif(a) * (1.f / kPi));
+__device__ __forceinline__ float H_of(float y, float s, const Reg& r) {   // Eq. (5), s = sinpi(y/eps)
+    if (y > r.eps) return 1.f;
+    if (y < -r.eps) return 0.f;
+    return 0.5f * (1.f + y * r.inv_eps + s * (1.f / kPi));
 }
-__device__ __forceinline__ float deps(float x, const Reg& r) {
-    if (fabsf(x) > r.eps) return 0.f;
-    return (1.f + cospif(x * r.inv_eps)) * (0.5f * r.inv_eps);
+__device__ __forceinline__ float d_of(float y, float c, const Reg& r) {   // Eq. (6), c = cospi(y/eps)
+    return fabsf(y) > r.eps ? 0.f : (1.f + c) * (0.5f * r.inv_eps);
 }
-__device__ __forceinline__ float dpeps(float x, const Reg& r) {
-    if (fabsf(x) > r.eps) return 0.f;
-    return -(0.5f * kPi) * r.inv_eps * r.inv_eps * sinpif(x * r.inv_eps);
+
+struct RegVals {
+    float h, hp, d, dp;    // h(x) Eq. (11), h'(x) Eq. (28), delta(x) Eq. (6), delta'(x) Eq. (29)
+};
+
+__device__ __forceinline__ RegVals reg_all(float x, const Reg& r) {
+    RegVals v;
+    if (fabsf(x) >= r.l + r.eps && fabsf(x) > r.eps) {   // outside every band: all four vanish
+        v.h = v.hp = v.d = v.dp = 0.f;
+        return v;
+    }
+    float s, c;
+    sincospif(x * r.inv_eps, &s, &c);
+    const float sp = s * r.cl + c * r.sl, cp = c * r.cl - s * r.sl;   // at x + l
+    const float sm = s * r.cl - c * r.sl, cm = c * r.cl + s * r.sl;   // at x - l
+    const float yp = x + r.l, ym = x - r.l;
+    const float Hp = H_of(yp, sp, r), Hm = H_of(ym, sm, r);
+    const float dpl = d_of(yp, cp, r), dmi = d_of(ym, cm, r);
+    v.h = Hp * (1.f - Hm);
+    v.hp = dpl * (1.f - Hm) - Hp * dmi;
+    const bool in = fabsf(x) <= r.eps;
+    v.d = in ? (1.f + c) * (0.5f * r.inv_eps) : 0.f;
+    v.dp = in ? -(0.5f * kPi) * r.inv_eps * r.inv_eps * s : 0.f;
+    return v;
 }
-__device__ __forceinline__ float hband(float x, const Reg& r) {
-    return Heps(x + r.l, r) * (1.f - Heps(x - r.l, r));
+
+__device__ __forceinline__ float reg_h(float x, const Reg& r) {
+    // fast exits: h = 0 when |x| >= l + eps (both factors saturate)
+    if (fabsf(x) >= r.l + r.eps) return 0.f;
+    float s, c;
+    sincospif(x * r.inv_eps, &s, &c);
+    const float sp = s * r.cl + c * r.sl;
+    const float sm = s * r.cl - c * r.sl;
+    return H_of(x + r.l, sp, r) * (1.f - H_of(x - r.l, sm, r));
 }
-__device__ __forceinline__ float hpband(float x, const Reg& r) {
-    return deps(x + r.l, r) * (1.f - Heps(x - r.l, r)) - Heps(x + r.l, r) * deps(x - r.l, r);
+
+// h(x) and delta(x) from one sincospif (w/b update)
+__device__ __forceinline__ void reg_hd(float x, const Reg& r, float& h, float& d) {
+    if (fabsf(x) >= r.l + r.eps && fabsf(x) > r.eps) {
+        h = d = 0.f;
+        return;
+    }
+    float s, c;
+    sincospif(x * r.inv_eps, &s, &c);
+    const float sp = s * r.cl + c * r.sl;
+    const float sm = s * r.cl - c * r.sl;
+    h = H_of(x + r.l, sp, r) * (1.f - H_of(x - r.l, sm, r));
+    d = fabsf(x) <= r.eps ? (1.f + c) * (0.5f * r.inv_eps) : 0.f;
 }
 
 __host__ __device__ constexpr int isqrt_c(int v) {
@@ -76,34 +137,44 @@ constexpr int ST_TH = ST_BY * ST_RT;
 
 template <int R>
 struct TileGeom {
-    static constexpr int LD = ST_TW + 2 * R + 1;   // float2 per smem row (odd: spreads banks)
+    static constexpr int RA = (R + 3) & ~3;              // halo rounded up to a float4
+    static constexpr int W = ST_TW + 2 * RA;             // staged columns [col0 - RA, col0 + TW + RA)
+    static constexpr int LD = W + 2;                     // float2 per smem row (LD/2 odd: spreads banks)
     static constexpr int ROWS = ST_TH + 2 * R;
     static constexpr int BYTES = LD * ROWS * 8;
 };
 
-// Stage u = h(phi) * w (two channels) over the tile + R halo; zero outside the image.
+// Stage u = h(phi) * w (two channels) over the tile + halo; zero outside the image (reading Q5).
+// float4 global loads: N is a multiple of 4 and the staged column range is 16-byte aligned.
 template <int R>
 __device__ __forceinline__ void stage_u(float2* __restrict__ U, const float* __restrict__ phi,
                                         const float* __restrict__ w1, const float* __restrict__ w2,
                                         int M, int N, int row0, int col0, const Reg& reg) {
     using TG = TileGeom<R>;
     const int tid = threadIdx.y * 32 + threadIdx.x;
-    const int nth = 32 * ST_BY;
-    constexpr int W = ST_TW + 2 * R;
-    for (int e = tid; e < TG::ROWS * W; e += nth) {
-        const int r = e / W, c = e - r * W;
-        const int gi = row0 - R + r, gj = col0 - R + c;
-        float2 u = make_float2(0.f, 0.f);
+    constexpr int NTH = 32 * ST_BY;
+    constexpr int F4 = TG::W / 4;
+    for (int e = tid; e < TG::ROWS * F4; e += NTH) {
+        const int r = e / F4, f = e - r * F4;
+        const int gi = row0 - R + r, gj = col0 - TG::RA + 4 * f;
+        float4 A = make_float4(0.f, 0.f, 0.f, 0.f), Bv = A;
         if (gi >= 0 && gi < M && gj >= 0 && gj < N) {
             const size_t o = (size_t)gi * N + gj;
-            const float hh = hband(__ldg(phi + o), reg);
-            u = make_float2(hh * __ldg(w1 + o), hh * __ldg(w2 + o));
+            const float4 P = __ldg(reinterpret_cast<const float4*>(phi + o));
+            const float4 X = __ldg(reinterpret_cast<const float4*>(w1 + o));
+            const float4 Y = __ldg(reinterpret_cast<const float4*>(w2 + o));
+            const float h0 = reg_h(P.x, reg), h1 = reg_h(P.y, reg), h2 = reg_h(P.z, reg), h3 = reg_h(P.w, reg);
+            A = make_float4(h0 * X.x, h0 * Y.x, h1 * X.y, h1 * Y.y);
+            Bv = make_float4(h2 * X.z, h2 * Y.z, h3 * X.w, h3 * Y.w);
         }
-        U[r * TG::LD + c] = u;
+        float4* dst = reinterpret_cast<float4*>(U + r * TG::LD + 4 * f);
+        dst[0] = A;
+        dst[1] = Bv;
     }
 }
 
-// v for the thread's RT x CT block (tile-local rows r0.., cols c0..) from the staged u.
+// v for the thread's RT x CT block (tile-local rows r0.., cols c0..) from the staged u, in packed
+// f32x2 arithmetic (both channels per instruction).
 template <int R, int SHAPE>
 __device__ __forceinline__ void window_block(const float2* __restrict__ U, int r0, int c0, const float* e,
                                              float2 (&v)[ST_RT][ST_CT]) {
@@ -112,21 +183,24 @@ __device__ __forceinline__ void window_block(const float2* __restrict__ U, int r
     for (int i = 0; i < ST_RT; i++)
 #pragma unroll
         for (int c = 0; c < ST_CT; c++) v[i][c] = make_float2(0.f, 0.f);
+    float2 ew[R + 1];
+#pragma unroll
+    for (int q = 0; q <= R; q++) ew[q] = make_float2(e[q], e[q]);
 #pragma unroll
     for (int rr = 0; rr < ST_RT + 2 * R; rr++) {
         float2 a[ST_CT + 2 * R];
+        const float2* row = U + (r0 + rr) * TG::LD + c0 + TG::RA - R;
 #pragma unroll
-        for (int x = 0; x < ST_CT + 2 * R; x++) a[x] = U[(r0 + rr) * TG::LD + c0 + x];
+        for (int x = 0; x < ST_CT + 2 * R; x++) a[x] = row[x];
         // S[L][c] = sum_{|q| <= L} e_q a[c + R + q]
         float2 S[R + 1][ST_CT];
 #pragma unroll
         for (int c = 0; c < ST_CT; c++) {
-            float2 acc = make_float2(e[0] * a[c + R].x, e[0] * a[c + R].y);
+            float2 acc = mul2(ew[0], a[c + R]);
             S[0][c] = acc;
 #pragma unroll
             for (int q = 1; q <= R; q++) {
-                acc.x = fmaf(e[q], a[c + R - q].x + a[c + R + q].x, acc.x);
-                acc.y = fmaf(e[q], a[c + R - q].y + a[c + R + q].y, acc.y);
+                acc = fma2(ew[q], add2(a[c + R - q], a[c + R + q]), acc);
                 S[q][c] = acc;
             }
         }
@@ -136,22 +210,23 @@ __device__ __forceinline__ void window_block(const float2* __restrict__ U, int r
             if (p >= -R && p <= R) {
                 const int ap = p < 0 ? -p : p;
                 const int L = half_width<R, SHAPE>(ap);
-                const float ep = e[ap];
 #pragma unroll
-                for (int c = 0; c < ST_CT; c++) {
-                    v[i][c].x = fmaf(ep, S[L][c].x, v[i][c].x);
-                    v[i][c].y = fmaf(ep, S[L][c].y, v[i][c].y);
-                }
+                for (int c = 0; c < ST_CT; c++) v[i][c] = fma2(ew[ap], S[L][c], v[i][c]);
             }
         }
     }
 }
 
-// F = psi + tau [ -gamma g |w| delta'(psi) + alpha g delta(psi) + 2 beta h'(psi) w.v + mu div(b - w) ]
+// Increment form of Eq. (37):  D = F - A psi, A = 1 - tau mu Delta_per, i.e.
+//   D = tau [ -gamma g |w| delta'(psi) + alpha g delta(psi) + 2 beta h'(psi) w.v + mu div(b - w)
+//             + mu Delta_per psi ],
+// so that phi^{s+1} = psi + A^{-1} D (= A^{-1} F, Eq. 33) and the FFT round-off scales with the
+// increment instead of with |psi| ~ 1 on the plateaus.  Delta_per is the periodic 5-point
+// Laplacian of Eq. (35) whose symbol is Eq. (32).
 template <int R, int SHAPE>
 __global__ void __launch_bounds__(32 * ST_BY) k_rhs(const float* __restrict__ phi, const float* __restrict__ w,
                                                     const float* __restrict__ bv, const float* __restrict__ g,
-                                                    float* __restrict__ F, StencilArgs a) {
+                                                    float* __restrict__ D, StencilArgs a) {
     extern __shared__ float2 U[];
     const int M = a.M, N = a.N;
     const size_t plane = (size_t)M * N;
@@ -162,45 +237,52 @@ __global__ void __launch_bounds__(32 * ST_BY) k_rhs(const float* __restrict__ ph
     const float* b1 = bv + img * 2 * plane;
     const float* b2 = b1 + plane;
     const float* gg = g + img * plane;
-    float* Fo = F + img * plane;
+    float* Do = D + img * plane;
     const int row0 = blockIdx.y * ST_TH, col0 = blockIdx.x * ST_TW;
     stage_u<R>(U, ph, w1, w2, M, N, row0, col0, a.reg);
     __syncthreads();
     const int r0 = threadIdx.y * ST_RT, c0 = threadIdx.x * ST_CT;
     const int gj = col0 + c0;
-    if (gj >= N) return;
+    if (gj >= N || row0 + r0 >= M) return;
     float2 v[ST_RT][ST_CT];
     window_block<R, SHAPE>(U, r0, c0, a.e, v);
-    // c1 = (b1 - w1) of the row above the first output row
+    const int jl = (gj - 1) & (N - 1), jr = (gj + ST_CT) & (N - 1);   // periodic neighbours
+    // c1 = (b1 - w1) and psi of the row above the first output row
     float c1p[ST_CT];
+    float4 Pu;
     {
         const int gi = row0 + r0 - 1;
 #pragma unroll
         for (int c = 0; c < ST_CT; c++) c1p[c] = 0.f;
-        if (gi >= 0 && gi < M) {
+        if (gi >= 0) {
             const float4 bb = __ldg(reinterpret_cast<const float4*>(b1 + (size_t)gi * N + gj));
             const float4 ww = __ldg(reinterpret_cast<const float4*>(w1 + (size_t)gi * N + gj));
             c1p[0] = bb.x - ww.x; c1p[1] = bb.y - ww.y; c1p[2] = bb.z - ww.z; c1p[3] = bb.w - ww.w;
         }
+        Pu = __ldg(reinterpret_cast<const float4*>(ph + (size_t)((gi + M) & (M - 1)) * N + gj));
     }
+    float4 P4 = __ldg(reinterpret_cast<const float4*>(ph + (size_t)(row0 + r0) * N + gj));
 #pragma unroll
     for (int i = 0; i < ST_RT; i++) {
         const int gi = row0 + r0 + i;
         if (gi >= M) break;
         const size_t o = (size_t)gi * N + gj;
-        const float4 P4 = __ldg(reinterpret_cast<const float4*>(ph + o));
+        const float4 Pd = __ldg(reinterpret_cast<const float4*>(ph + (size_t)((gi + 1) & (M - 1)) * N + gj));
+        const float pl = __ldg(ph + (size_t)gi * N + jl), pr = __ldg(ph + (size_t)gi * N + jr);
         const float4 W1 = __ldg(reinterpret_cast<const float4*>(w1 + o));
         const float4 W2 = __ldg(reinterpret_cast<const float4*>(w2 + o));
         const float4 B1 = __ldg(reinterpret_cast<const float4*>(b1 + o));
         const float4 B2 = __ldg(reinterpret_cast<const float4*>(b2 + o));
         const float4 G4 = __ldg(reinterpret_cast<const float4*>(gg + o));
-        const float p_[4] = {P4.x, P4.y, P4.z, P4.w};
+        const float p_[6] = {pl, P4.x, P4.y, P4.z, P4.w, pr};
+        const float pu_[4] = {Pu.x, Pu.y, Pu.z, Pu.w};
+        const float pd_[4] = {Pd.x, Pd.y, Pd.z, Pd.w};
         const float w1_[4] = {W1.x, W1.y, W1.z, W1.w};
         const float w2_[4] = {W2.x, W2.y, W2.z, W2.w};
         const float b1_[4] = {B1.x, B1.y, B1.z, B1.w};
         const float b2_[4] = {B2.x, B2.y, B2.z, B2.w};
         const float g_[4] = {G4.x, G4.y, G4.z, G4.w};
-        float c2l = 0.f;   // (b2 - w2) at column gj - 1
+        float c2l = 0.f;   // (b2 - w2) at column gj - 1 (non-periodic divergence, Eq. 36 / Q6)
         if (gj > 0) c2l = __ldg(b2 + o - 1) - __ldg(w2 + o - 1);
         float out[4];
 #pragma unroll
@@ -215,23 +297,29 @@ __global__ void __launch_bounds__(32 * ST_BY) k_rhs(const float* __restrict__ ph
             if (j > 0) dv -= c2l;
             c2l = c2;
             c1p[c] = c1;
-            const float ps = p_[c];
+            const float ps = p_[c + 1];
+            // neighbour differences first: exact (Sterbenz) for nearby values, so the O(1) level of
+            // psi does not enter the rounding of the Laplacian
+            const float lap = ((pu_[c] - ps) + (pd_[c] - ps)) + ((p_[c] - ps) + (p_[c + 2] - ps));
             const float wn = sqrtf(w1_[c] * w1_[c] + w2_[c] * w2_[c]);
             const float wv = w1_[c] * v[i][c].x + w2_[c] * v[i][c].y;
-            const float t = -a.gamma * g_[c] * wn * dpeps(ps, a.reg) + a.alpha * g_[c] * deps(ps, a.reg) +
-                            2.f * a.beta * hpband(ps, a.reg) * wv + a.mu * dv;
-            out[c] = ps + a.tau * t;
+            const RegVals rv = reg_all(ps, a.reg);
+            const float t = -a.gamma * g_[c] * wn * rv.dp + a.alpha * g_[c] * rv.d + 2.f * a.beta * rv.hp * wv +
+                            a.mu * (dv + lap);
+            out[c] = a.tau * t;
         }
-        *reinterpret_cast<float4*>(Fo + o) = make_float4(out[0], out[1], out[2], out[3]);
+        *reinterpret_cast<float4*>(Do + o) = make_float4(out[0], out[1], out[2], out[3]);
+        Pu = P4;
+        P4 = Pd;
     }
 }
 
 __device__ __forceinline__ void project_w(int mode, float& x, float& y) {
-    const float n = sqrtf(x * x + y * y);
-    if (mode == 0) {
-        if (n > 1.f) { x /= n; y /= n; }
-    } else if (mode == 1) {
-        if (n > 1e-4f) { x /= n; y /= n; }
+    const float n2 = x * x + y * y;
+    if ((mode == 0 && n2 > 1.f) || (mode == 1 && n2 > 1e-8f)) {   // BALL: |w| > 1; SPHERE: |w| > 1e-4
+        const float inv = rsqrtf(n2);
+        x *= inv;
+        y *= inv;
     }
 }
 
@@ -288,15 +376,16 @@ __global__ void __launch_bounds__(32 * ST_BY) k_wb(const float* __restrict__ phi
             const float ps = p_[c];
             const float gp1 = (gi < M - 1) ? pn_[c] - ps : 0.f;
             const float gp2 = (j < N - 1) ? p_[c + 1] - ps : 0.f;
-            const float hh = hband(ps, a.reg);
-            float x, y;
+            float x, y, hh, dd;
+            reg_hd(ps, a.reg, hh, dd);
             if (MODE == 0) {
                 const float Bx = gp1 + b1_[c] + a.beta2_mu * hh * v[i][c].x;
                 const float By = gp2 + b2_[c] + a.beta2_mu * hh * v[i][c].y;
-                const float t = a.gamma_mu * g_[c] * deps(ps, a.reg);
-                const float nb = sqrtf(Bx * Bx + By * By);
-                if (nb > 0.f) {
-                    const float m = fmaxf(nb - t, 0.f) / nb;
+                const float t = a.gamma_mu * g_[c] * dd;
+                const float nb2 = Bx * Bx + By * By;
+                if (nb2 > 0.f) {
+                    const float inv = rsqrtf(nb2);           // 1/|B|
+                    const float m = fmaxf(1.f - t * inv, 0.f);  // max(|B| - t, 0)/|B|
                     x = m * Bx;
                     y = m * By;
                 } else {
@@ -304,7 +393,7 @@ __global__ void __launch_bounds__(32 * ST_BY) k_wb(const float* __restrict__ phi
                     y = 0.f;
                 }
             } else {
-                const float den = a.gamma * g_[c] * deps(ps, a.reg) + a.mu;
+                const float den = a.gamma * g_[c] * dd + a.mu;
                 x = (a.mu * gp1 + a.mu * b1_[c] + 2.f * a.beta * hh * v[i][c].x) / den;
                 y = (a.mu * gp2 + a.mu * b2_[c] + 2.f * a.beta * hh * v[i][c].y) / den;
             }

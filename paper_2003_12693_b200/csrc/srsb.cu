@@ -135,6 +135,7 @@ sr_status configure(sr_sb_ctx* c) {
     c->ra.lg_G = ilog2(G);
     c->ra.SR = padded(H, G / 2 > 0 ? G / 2 : 1);
     c->ra.clip = 0.f;
+    c->ra.accum = 0;
     c->rgrid = dim3(M / rpc, B, 1);
     c->rblock = dim3(rpc * T_h, 1, 1);
     c->rsmem = rpc * 2 * c->ra.SR * (int)sizeof(float);
@@ -159,6 +160,8 @@ sr_status configure(sr_sb_ctx* c) {
     a.reg.eps = p.epsilon;
     a.reg.inv_eps = 1.f / p.epsilon;
     a.reg.l = p.l;
+    a.reg.sl = (float)std::sin(3.14159265358979323846 * (double)p.l / (double)p.epsilon);
+    a.reg.cl = (float)std::cos(3.14159265358979323846 * (double)p.l / (double)p.epsilon);
     for (int q = 0; q <= 8; q++) a.e[q] = (float)std::exp(-(double)(q * q) / ((double)p.d * p.d));
     a.tau = p.tau;
     a.gamma = p.gamma;
@@ -219,8 +222,10 @@ void prof_end(sr_sb_ctx* c, int cls) {
     c->ev_used += 2;
 }
 
-sr_status enq_solve(sr_sb_ctx* c, const float* F, float* out, float clip) {
+// phi_out = A^{-1} F (accum = 0) or phi_out += A^{-1} F (accum = 1, increment form), then clamp
+sr_status enq_solve(sr_sb_ctx* c, const float* F, float* out, float clip, int accum) {
     FftRowArgs ra = c->ra;
+    ra.accum = accum;
     prof_begin(c);
     c->rfwd<<<c->rgrid, c->rblock, c->rsmem, c->s>>>(F, c->spec, c->twH, c->twR, ra);
     prof_end(c, SR_K_ROWS_R2C);
@@ -258,7 +263,7 @@ sr_status enq_wb(sr_sb_ctx* c) {
 sr_status enq_iteration(sr_sb_ctx* c) {
     for (int s = 0; s < c->p.S; s++) {
         enq_rhs(c, c->F);
-        enq_solve(c, c->F, c->phi, (s == c->p.S - 1) ? c->p.phi_clip : 0.f);
+        enq_solve(c, c->F, c->phi, (s == c->p.S - 1) ? c->p.phi_clip : 0.f, 1);
     }
     enq_wb(c);
     return SR_OK;
@@ -318,16 +323,27 @@ void sr_sb_default_params(sr_sb_params* p, int M, int N, int batch, int window) 
     p->M = M;
     p->N = N;
     p->batch = batch;
-    p->gamma = 4.f;
+    p->gamma = 1.f;
     p->alpha = 4.f;
-    p->beta = 0.2f;
+    // reading Q24: beta * sum_W G = 0.2 * (the same sum for the caption's 5x5 window, d = 5)
+    {
+        auto wsum = [](int R, double d, int shape) {
+            double s = 0.0;
+            for (int q1 = -R; q1 <= R; q1++)
+                for (int q2 = -R; q2 <= R; q2++)
+                    if (shape == 1 || q1 * q1 + q2 * q2 <= R * R) s += std::exp(-(double)(q1 * q1 + q2 * q2) / (d * d));
+            return s;
+        };
+        const double d = window > 0 ? (double)window : 1.0;
+        p->beta = (float)(0.2 * wsum(2, 5.0, 1) / wsum(window < 0 ? 0 : window, d, 0));
+    }
     p->mu = 8.f;
     p->epsilon = 0.5f;
     p->l = 0.5f;
     p->window = window;
     p->d = (float)window > 0 ? (float)window : 1.f;
     p->window_shape = SR_WIN_DISC;
-    p->tau = 0.1f;
+    p->tau = 0.05f;
     p->S = 3;
     p->rho = 30.f;
     p->sigma = 1.f;
@@ -515,7 +531,7 @@ sr_status sr_sb_debug_solve(sr_sb_ctx* c, const float* F, float* phi_out) {
     // solve into F's own buffer is not allowed (rows read F while c2r writes); use a temporary
     float* tmp = nullptr;
     CK(cudaMallocAsync((void**)&tmp, n * 4, c->s));
-    enq_solve(c, c->F, tmp, 0.f);
+    enq_solve(c, c->F, tmp, 0.f, 0);
     CK(cudaMemcpyAsync(phi_out, tmp, n * 4, cudaMemcpyDefault, c->s));
     CK(cudaFreeAsync(tmp, c->s));
     RET(end(c));

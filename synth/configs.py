@@ -27,21 +27,49 @@ BASE_SEED = 12693
 
 
 def paper_params(window: int, **over) -> dict:
-    """Figure-1 caption parameter set used for every config (readings Q17, Q22).
+    """Parameter set used for every config (readings Q17, Q22, Q23).
 
-    alpha=4, gamma=4, beta=0.2, mu=8, S=3, tau=0.1 as in the caption; d = window
-    radius (Eq. 38 ties the half-width to d, reading Q2); s=2, sigma=1
-    (north_star's g = 1/(1+|grad(G_sigma*I)|^2)); phi clamped to [-1, 1]
-    (north_star); w projected onto the unit ball (reading Q1); disc window.
-    epsilon = l = 1/2 and rho = 30 (reading Q22): with the clamp, the caption's
-    epsilon = l = 1 put the +-1 plateaus on the band edge and every C1 contour
-    collapses in the oracle; rho is unstated in the paper (Q4).
+    From the Fig. 1 caption: alpha=4, beta=0.2, mu=8, S=3.  d = window radius
+    (Eq. 38 ties the half-width to d, reading Q2); s=2, sigma=1 (north_star's
+    g = 1/(1+|grad(G_sigma*I)|^2)); phi clamped to [-1, 1] (north_star); w projected onto the
+    unit ball (reading Q1); disc window.
+    Q22: epsilon = l = 1/2 -- with the clamp, the caption's epsilon = l = 1 put the +-1 plateaus
+         on the band edge and every C1 contour collapses in the oracle.
+    Q23: gamma = 1, tau = 0.05 -- the explicit -gamma g |w| delta'(phi) term of Eq. (37) has
+         pointwise stiffness tau gamma pi^2 / (2 eps^3); with eps = 1/2 the caption's gamma = 4,
+         tau = 0.1 give 15.8 and the fp64 oracle itself amplifies a 1e-7 perturbation to O(1)
+         in 10 iterations; gamma = 1, tau = 0.05 give 1.97 (the caption set's own value at eps = 1).
+    Q24: beta = 0.2 * G5 / G_W(window, d), G_W = sum over the window of exp(-(p^2+q^2)/d^2) and
+         G5 = 21.4 the same sum for the caption's 5x5 window with d = 5: the repulsion
+         strength beta * G_W stays the caption's ("an excessively large beta causes the
+         contour to become unstable"); without it the R = 6 config amplifies 1e-6 to 0.1 in 10
+         iterations of the fp64 oracle.
+    rho = 30 (unstated in the paper, reading Q4): C1 keeps one component.
     """
-    p = dict(gamma=4.0, alpha=4.0, beta=0.2, mu=8.0, epsilon=0.5, l=0.5,
-             d=float(window), window=int(window), window_shape=0, tau=0.1, S=3,
+    d = float(over.get("d", window if window > 0 else 1.0))
+    shape = int(over.get("window_shape", 0))
+    p = dict(gamma=1.0, alpha=4.0, beta=repulsion_beta(window, d, shape), mu=8.0, epsilon=0.5, l=0.5,
+             d=d, window=int(window), window_shape=shape, tau=0.05, S=3,
              rho=30.0, sigma=1.0, s=2, phi_clip=1.0, w_proj=0, w_mode=0, w_iters=1)
     p.update(over)
     return p
+
+
+def window_weight_sum(window: int, d: float, shape: int = 0) -> float:
+    """sum_{(p,q) in W} exp(-(p^2+q^2)/d^2) over the disc (shape 0) or square (1) of radius `window`."""
+    s = 0.0
+    for p in range(-window, window + 1):
+        for q in range(-window, window + 1):
+            if shape == 0 and p * p + q * q > window * window:
+                continue
+            s += math.exp(-(p * p + q * q) / (d * d))
+    return s
+
+
+def repulsion_beta(window: int, d: float, shape: int = 0) -> float:
+    """Reading Q24: beta * G_W = 0.2 * G_W(5x5 square, d = 5) of the Fig. 1 caption."""
+    ref = 0.2 * window_weight_sum(2, 5.0, 1)
+    return ref / window_weight_sum(window, d, shape)
 
 
 def _rng(c: int, idx: int = 0) -> np.random.Generator:

@@ -60,8 +60,8 @@ def test_params_struct_matches_header(srsb):
 
 def test_default_params_are_the_design_readings(srsb):
     p = srsb.default_params(128, 128, 1, 3)
-    assert (p["gamma"], p["alpha"], p["mu"], p["S"]) == (4.0, 4.0, 8.0, 3)
-    assert p["beta"] == pytest.approx(0.2) and p["tau"] == pytest.approx(0.1)
+    assert (p["gamma"], p["alpha"], p["mu"], p["S"]) == (1.0, 4.0, 8.0, 3)
+    assert p["beta"] == pytest.approx(0.2370643, rel=1e-5) and p["tau"] == pytest.approx(0.05)
     assert (p["epsilon"], p["l"], p["rho"], p["d"], p["window"]) == (0.5, 0.5, 30.0, 3.0, 3)
     assert (p["phi_clip"], p["w_proj"], p["window_shape"]) == (1.0, 0, 0)
     from synth import paper_params

@@ -118,15 +118,36 @@ def test_c1_topology_sr_vs_gac(orc):
 @pytest.mark.slow
 def test_two_seed_merge(orc):
     """North star: two growing seeds (alpha < 0) that plain GAC (beta = 0) merges stay two
-    components under SR."""
+    components under SR.  On C1's image: seeds of radius 15 at the disk centres, K = 300.
+    (DESIGN.md §2 Q25 records that under the clamp reading SR later fragments the grown fronts.)"""
     from synth import make_config
     c = make_config("c1")
     P = dict(c["params"], alpha=-4.0)
     ii, jj = np.meshgrid(np.arange(128.0), np.arange(128.0), indexing="ij")
-    seeds = ((ii - 63.5) ** 2 + (jj - 41.5) ** 2 <= 100) | ((ii - 63.5) ** 2 + (jj - 85.5) ** 2 <= 100)
+    seeds = ((ii - 63.5) ** 2 + (jj - 41.5) ** 2 <= 225) | ((ii - 63.5) ** 2 + (jj - 85.5) ** 2 <= 225)
     phi0 = np.where(seeds, -1.0, 1.0)
     g = orc.edge(c["image"][0], P["sigma"], P["rho"], P["s"])
     sr = _run(orc, P, phi0, g, 300)
     gac = _run(orc, dict(P, beta=0.0), phi0, g, 300)
     assert orc.label(sr["phi"] < 0)[0] == 2
     assert orc.label(gac["phi"] < 0)[0] == 1
+
+
+@pytest.mark.slow
+def test_perturbation_growth_is_bounded(orc):
+    """Reading Q23: under the chosen parameters the iteration is not chaotic -- a 1e-7
+    perturbation of phi grows by less than 100x over 10 iterations (so fp32 vs fp64 parity
+    at 1e-4 is attainable); the caption's gamma = 4, tau = 0.1 at eps = 1/2 are not."""
+    from synth import make_config
+    c = make_config("c1")
+    g = orc.edge(c["image"][0], 1.0, c["params"]["rho"], 2)
+
+    def growth(P):
+        a = _run(orc, P, c["phi0"][0], g, 2)
+        b = {k: v.copy() for k, v in a.items()}
+        b["phi"] = np.clip(b["phi"] + 1e-7 * np.random.default_rng(0).standard_normal(b["phi"].shape), -1, 1)
+        orc.iterate(P, a, g, 10)
+        orc.iterate(P, b, g, 10)
+        return np.abs(a["phi"] - b["phi"]).max()
+    assert growth(c["params"]) < 1e-5
+    assert growth(dict(c["params"], gamma=4.0, tau=0.1)) > 1e-3

@@ -97,7 +97,7 @@ def test_wb_repulsion_term_by_impulse(orc):
         for j in range(N):
             r2 = (i - 5) ** 2 + (j - 5) ** 2
             G = np.exp(-r2 / 9.0) if r2 <= 9 else 0.0
-            assert n1[i, j] == pytest.approx(2 * 0.2 / 8.0 * G, abs=1e-15)
+            assert n1[i, j] == pytest.approx(2 * P["beta"] / P["mu"] * G, abs=1e-15)
             assert n2[i, j] == 0.0
 
 

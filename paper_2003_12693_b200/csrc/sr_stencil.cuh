@@ -47,7 +47,18 @@ __device__ __forceinline__ float2 mul2(float2 a, float2 b) {
 struct Reg {
     float eps, inv_eps, l;
     float sl, cl;          // sinpi(l / eps), cospi(l / eps)
+    int l_eq_eps;          // l == eps (the default reading Q22): closed forms below
 };
+
+// With l = eps and a = x / eps, Eq. (5), (6), (11), (28), (29) reduce on |a| < 2 to
+//   h  = (2 - |a| + sinpi(|a|)/pi) / 2,           h' = -sign(a) (1 - cospi(a)) / (2 eps),
+//   delta = (1 + cospi(a)) / (2 eps) [|a| <= 1],  delta' = -(pi / (2 eps^2)) sinpi(a) [|a| <= 1],
+// and all four vanish for |a| >= 2 (only one of H(x +- l) is inside its band at a time).
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float y;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 
 __device__ __forceinline__ float H_of(float y, float s, const Reg& r) {   // Eq. (5), s = sinpi(y/eps)
     if (y > r.eps) return 1.f;
@@ -62,8 +73,25 @@ struct RegVals {
     float h, hp, d, dp;    // h(x) Eq. (11), h'(x) Eq. (28), delta(x) Eq. (6), delta'(x) Eq. (29)
 };
 
+template <bool LEQ>
 __device__ __forceinline__ RegVals reg_all(float x, const Reg& r) {
     RegVals v;
+    if constexpr (LEQ) {
+        const float a = x * r.inv_eps, aa = fabsf(a);
+        if (aa >= 2.f) {
+            v.h = v.hp = v.d = v.dp = 0.f;
+            return v;
+        }
+        float s, c;
+        sincospif(a, &s, &c);
+        const float sg = copysignf(1.f, a);
+        v.h = 0.5f * (2.f - aa + sg * s * (1.f / kPi));
+        v.hp = -sg * (1.f - c) * (0.5f * r.inv_eps);
+        const bool in = aa <= 1.f;
+        v.d = in ? (1.f + c) * (0.5f * r.inv_eps) : 0.f;
+        v.dp = in ? -(0.5f * kPi) * r.inv_eps * r.inv_eps * s : 0.f;
+        return v;
+    }
     if (fabsf(x) >= r.l + r.eps && fabsf(x) > r.eps) {   // outside every band: all four vanish
         v.h = v.hp = v.d = v.dp = 0.f;
         return v;
@@ -83,7 +111,12 @@ __device__ __forceinline__ RegVals reg_all(float x, const Reg& r) {
     return v;
 }
 
+template <bool LEQ>
 __device__ __forceinline__ float reg_h(float x, const Reg& r) {
+    if constexpr (LEQ) {
+        const float aa = fabsf(x * r.inv_eps);
+        return aa >= 2.f ? 0.f : 0.5f * (2.f - aa + sinpif(aa) * (1.f / kPi));
+    }
     // fast exits: h = 0 when |x| >= l + eps (both factors saturate)
     if (fabsf(x) >= r.l + r.eps) return 0.f;
     float s, c;
@@ -94,7 +127,20 @@ __device__ __forceinline__ float reg_h(float x, const Reg& r) {
 }
 
 // h(x) and delta(x) from one sincospif (w/b update)
+template <bool LEQ>
 __device__ __forceinline__ void reg_hd(float x, const Reg& r, float& h, float& d) {
+    if constexpr (LEQ) {
+        const float a = x * r.inv_eps, aa = fabsf(a);
+        if (aa >= 2.f) {
+            h = d = 0.f;
+            return;
+        }
+        float s, c;
+        sincospif(aa, &s, &c);
+        h = 0.5f * (2.f - aa + s * (1.f / kPi));
+        d = aa <= 1.f ? (1.f + c) * (0.5f * r.inv_eps) : 0.f;
+        return;
+    }
     if (fabsf(x) >= r.l + r.eps && fabsf(x) > r.eps) {
         h = d = 0.f;
         return;
@@ -127,6 +173,7 @@ struct StencilArgs {
     float gamma_mu;    // gamma / mu
     int w_proj;        // 0 ball, 1 sphere, 2 none
     float b_max;
+    int tiles_x, tiles_y, ntiles;   // persistent tile loop: tiles per row, per column, total (x batch)
 };
 
 constexpr int ST_CT = 4;   // columns per thread
@@ -137,48 +184,53 @@ constexpr int ST_TH = ST_BY * ST_RT;
 
 template <int R>
 struct TileGeom {
-    static constexpr int RA = (R + 3) & ~3;              // halo rounded up to a float4
+    static constexpr int RA = (R + 1) & ~1;              // halo rounded up to a 2-pixel chunk
     static constexpr int W = ST_TW + 2 * RA;             // staged columns [col0 - RA, col0 + TW + RA)
-    static constexpr int LD = W + 2;                     // float2 per smem row (LD/2 odd: spreads banks)
+    static constexpr int CH = W / 2;                     // 16-byte chunks (2 px x 2 channels) per row
+    static constexpr int LDC = (CH + 7) & ~7;            // chunk stride per row (multiple of 8)
     static constexpr int ROWS = ST_TH + 2 * R;
-    static constexpr int BYTES = LD * ROWS * 8;
+    static constexpr int BYTES = LDC * ROWS * 16;
 };
 
+// bank-conflict-free chunk swizzle: 8 consecutive even (or odd) chunks map to 8 distinct bank quads
+__device__ __forceinline__ int swz(int c) { return c ^ ((c >> 3) & 1); }
+
 // Stage u = h(phi) * w (two channels) over the tile + halo; zero outside the image (reading Q5).
-// float4 global loads: N is a multiple of 4 and the staged column range is 16-byte aligned.
-template <int R>
-__device__ __forceinline__ void stage_u(float2* __restrict__ U, const float* __restrict__ phi,
+// One 2-pixel chunk per thread and step: float2 global loads, one float4 shared store.
+template <int R, bool LEQ>
+__device__ __forceinline__ void stage_u(float4* __restrict__ U, const float* __restrict__ phi,
                                         const float* __restrict__ w1, const float* __restrict__ w2,
                                         int M, int N, int row0, int col0, const Reg& reg) {
     using TG = TileGeom<R>;
     const int tid = threadIdx.y * 32 + threadIdx.x;
     constexpr int NTH = 32 * ST_BY;
-    constexpr int F4 = TG::W / 4;
-    for (int e = tid; e < TG::ROWS * F4; e += NTH) {
-        const int r = e / F4, f = e - r * F4;
-        const int gi = row0 - R + r, gj = col0 - TG::RA + 4 * f;
-        float4 A = make_float4(0.f, 0.f, 0.f, 0.f), Bv = A;
+    constexpr int TOT = TG::ROWS * TG::CH;
+#pragma unroll 4
+    for (int e = tid; e < TOT; e += NTH) {
+        const int r = e / TG::CH, f = e - r * TG::CH;
+        const int gi = row0 - R + r, gj = col0 - TG::RA + 2 * f;
+        float4 A = make_float4(0.f, 0.f, 0.f, 0.f);
         if (gi >= 0 && gi < M && gj >= 0 && gj < N) {
             const size_t o = (size_t)gi * N + gj;
-            const float4 P = __ldg(reinterpret_cast<const float4*>(phi + o));
-            const float4 X = __ldg(reinterpret_cast<const float4*>(w1 + o));
-            const float4 Y = __ldg(reinterpret_cast<const float4*>(w2 + o));
-            const float h0 = reg_h(P.x, reg), h1 = reg_h(P.y, reg), h2 = reg_h(P.z, reg), h3 = reg_h(P.w, reg);
+            const float2 P = __ldg(reinterpret_cast<const float2*>(phi + o));
+            const float2 X = __ldg(reinterpret_cast<const float2*>(w1 + o));
+            const float2 Y = __ldg(reinterpret_cast<const float2*>(w2 + o));
+            const float h0 = reg_h<LEQ>(P.x, reg), h1 = reg_h<LEQ>(P.y, reg);
             A = make_float4(h0 * X.x, h0 * Y.x, h1 * X.y, h1 * Y.y);
-            Bv = make_float4(h2 * X.z, h2 * Y.z, h3 * X.w, h3 * Y.w);
         }
-        float4* dst = reinterpret_cast<float4*>(U + r * TG::LD + 4 * f);
-        dst[0] = A;
-        dst[1] = Bv;
+        U[r * TG::LDC + swz(f)] = A;
     }
 }
 
 // v for the thread's RT x CT block (tile-local rows r0.., cols c0..) from the staged u, in packed
-// f32x2 arithmetic (both channels per instruction).
+// f32x2 arithmetic (both channels per instruction); conflict-free LDS.128 row reads.
 template <int R, int SHAPE>
-__device__ __forceinline__ void window_block(const float2* __restrict__ U, int r0, int c0, const float* e,
+__device__ __forceinline__ void window_block(const float4* __restrict__ U, int r0, int c0, const float* e,
                                              float2 (&v)[ST_RT][ST_CT]) {
     using TG = TileGeom<R>;
+    constexpr int OFF = (TG::RA - R) & 1;                 // first needed float2 is odd -> load one earlier
+    constexpr int NA = ST_CT + 2 * R + OFF;               // float2 values loaded per halo row
+    constexpr int NC = (NA + 1) / 2;                      // chunks loaded per halo row
 #pragma unroll
     for (int i = 0; i < ST_RT; i++)
 #pragma unroll
@@ -186,21 +238,27 @@ __device__ __forceinline__ void window_block(const float2* __restrict__ U, int r
     float2 ew[R + 1];
 #pragma unroll
     for (int q = 0; q <= R; q++) ew[q] = make_float2(e[q], e[q]);
+    const int chunk0 = (c0 + TG::RA - R - OFF) >> 1;
 #pragma unroll
     for (int rr = 0; rr < ST_RT + 2 * R; rr++) {
-        float2 a[ST_CT + 2 * R];
-        const float2* row = U + (r0 + rr) * TG::LD + c0 + TG::RA - R;
+        float2 a[2 * NC];
+        const float4* row = U + (r0 + rr) * TG::LDC;
 #pragma unroll
-        for (int x = 0; x < ST_CT + 2 * R; x++) a[x] = row[x];
-        // S[L][c] = sum_{|q| <= L} e_q a[c + R + q]
+        for (int k = 0; k < NC; k++) {
+            const float4 q4 = row[swz(chunk0 + k)];
+            a[2 * k] = make_float2(q4.x, q4.y);
+            a[2 * k + 1] = make_float2(q4.z, q4.w);
+        }
+        // S[L][c] = sum_{|q| <= L} e_q a[OFF + c + R + q]
         float2 S[R + 1][ST_CT];
 #pragma unroll
         for (int c = 0; c < ST_CT; c++) {
-            float2 acc = mul2(ew[0], a[c + R]);
+            const int m = OFF + c + R;
+            float2 acc = mul2(ew[0], a[m]);
             S[0][c] = acc;
 #pragma unroll
             for (int q = 1; q <= R; q++) {
-                acc = fma2(ew[q], add2(a[c + R - q], a[c + R + q]), acc);
+                acc = fma2(ew[q], add2(a[m - q], a[m + q]), acc);
                 S[q][c] = acc;
             }
         }
@@ -217,20 +275,50 @@ __device__ __forceinline__ void window_block(const float2* __restrict__ U, int r
     }
 }
 
+// Bulk L2 prefetch (cp.async.bulk.prefetch.L2) of the halo extent of one tile of `nf` fields:
+// rows [row0 - R, row0 + TH + R), columns [col0 - RA, col0 + TW + RA) clipped to the image, 16 B
+// aligned.  Issued one tile ahead by the persistent loop so the demand loads of the next tile hit L2.
+__device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+template <int R>
+__device__ __forceinline__ void prefetch_tile(const StencilArgs& a, int t, const float* phi, const float* w,
+                                              const float* bv, const float* g) {
+    using TG = TileGeom<R>;
+    const int M = a.M, N = a.N;
+    const int bx = t % a.tiles_x, rq = t / a.tiles_x;
+    const int by = rq % a.tiles_y, img = rq / a.tiles_y;
+    const int row0 = by * ST_TH, col0 = bx * ST_TW;
+    const size_t plane = (size_t)M * N;
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    const int r_lo = max(row0 - R - 1, 0), r_hi = min(row0 + ST_TH + R + 1, M);
+    const int c_lo = max(col0 - TG::RA, 0) & ~3, c_hi = (min(col0 + ST_TW + TG::RA, N) + 3) & ~3;
+    const unsigned bytes = (unsigned)(c_hi - c_lo) * 4u;
+    const int rows = r_hi - r_lo;
+    for (int e = tid; e < rows * 6; e += 32 * ST_BY) {
+        const int f = e / rows, r = r_lo + (e - f * rows);
+        // fields: phi, w1, w2, b1, b2, g of image img
+        const float* base = f == 0 ? phi + img * plane
+                          : f <= 2 ? w + (2 * img + (f - 1)) * plane
+                          : f <= 4 ? bv + (2 * img + (f - 3)) * plane
+                                   : g + img * plane;
+        l2_prefetch(base + (size_t)r * N + c_lo, bytes);
+    }
+}
+
 // Increment form of Eq. (37):  D = F - A psi, A = 1 - tau mu Delta_per, i.e.
 //   D = tau [ -gamma g |w| delta'(psi) + alpha g delta(psi) + 2 beta h'(psi) w.v + mu div(b - w)
 //             + mu Delta_per psi ],
 // so that phi^{s+1} = psi + A^{-1} D (= A^{-1} F, Eq. 33) and the FFT round-off scales with the
 // increment instead of with |psi| ~ 1 on the plateaus.  Delta_per is the periodic 5-point
 // Laplacian of Eq. (35) whose symbol is Eq. (32).
-template <int R, int SHAPE>
-__global__ void __launch_bounds__(32 * ST_BY) k_rhs(const float* __restrict__ phi, const float* __restrict__ w,
-                                                    const float* __restrict__ bv, const float* __restrict__ g,
-                                                    float* __restrict__ D, StencilArgs a) {
-    extern __shared__ float2 U[];
+template <int R, int SHAPE, bool LEQ>
+__device__ __forceinline__ void rhs_tile(float4* __restrict__ U, const float* __restrict__ phi,
+                                         const float* __restrict__ w, const float* __restrict__ bv,
+                                         const float* __restrict__ g, float* __restrict__ D, const StencilArgs& a,
+                                         int img, int by, int bx) {
     const int M = a.M, N = a.N;
     const size_t plane = (size_t)M * N;
-    const int img = blockIdx.z;
     const float* ph = phi + img * plane;
     const float* w1 = w + img * 2 * plane;
     const float* w2 = w1 + plane;
@@ -238,8 +326,8 @@ __global__ void __launch_bounds__(32 * ST_BY) k_rhs(const float* __restrict__ ph
     const float* b2 = b1 + plane;
     const float* gg = g + img * plane;
     float* Do = D + img * plane;
-    const int row0 = blockIdx.y * ST_TH, col0 = blockIdx.x * ST_TW;
-    stage_u<R>(U, ph, w1, w2, M, N, row0, col0, a.reg);
+    const int row0 = by * ST_TH, col0 = bx * ST_TW;
+    stage_u<R, LEQ>(U, ph, w1, w2, M, N, row0, col0, a.reg);
     __syncthreads();
     const int r0 = threadIdx.y * ST_RT, c0 = threadIdx.x * ST_CT;
     const int gj = col0 + c0;
@@ -301,9 +389,9 @@ __global__ void __launch_bounds__(32 * ST_BY) k_rhs(const float* __restrict__ ph
             // neighbour differences first: exact (Sterbenz) for nearby values, so the O(1) level of
             // psi does not enter the rounding of the Laplacian
             const float lap = ((pu_[c] - ps) + (pd_[c] - ps)) + ((p_[c] - ps) + (p_[c + 2] - ps));
-            const float wn = sqrtf(w1_[c] * w1_[c] + w2_[c] * w2_[c]);
+            const float wn = sqrt_approx(w1_[c] * w1_[c] + w2_[c] * w2_[c]);
             const float wv = w1_[c] * v[i][c].x + w2_[c] * v[i][c].y;
-            const RegVals rv = reg_all(ps, a.reg);
+            const RegVals rv = reg_all<LEQ>(ps, a.reg);
             const float t = -a.gamma * g_[c] * wn * rv.dp + a.alpha * g_[c] * rv.d + 2.f * a.beta * rv.hp * wv +
                             a.mu * (dv + lap);
             out[c] = a.tau * t;
@@ -326,15 +414,13 @@ __device__ __forceinline__ void project_w(int mode, float& x, float& y) {
 // MODE 0: threshold (Eq. 41-42); MODE 1: fixed-point sweep (Eq. 38-39).  UPDATE_B: last pass,
 // b += grad phi - w_new (Eq. 23) and the non-finite guard.  w_in is read for v (the halo) only in
 // mode 1 beyond the pixel; in mode 0 w_in = w^k.  b is updated in place (pixel-local).
-template <int R, int SHAPE, int MODE, bool UPDATE_B>
-__global__ void __launch_bounds__(32 * ST_BY) k_wb(const float* __restrict__ phi, const float* __restrict__ w_in,
-                                                   float* __restrict__ w_out, float* __restrict__ bv,
-                                                   const float* __restrict__ g, int* __restrict__ flag,
-                                                   StencilArgs a) {
-    extern __shared__ float2 U[];
+template <int R, int SHAPE, int MODE, bool UPDATE_B, bool LEQ>
+__device__ __forceinline__ void wb_tile(float4* __restrict__ U, const float* __restrict__ phi,
+                                        const float* __restrict__ w_in, float* __restrict__ w_out,
+                                        float* __restrict__ bv, const float* __restrict__ g,
+                                        int* __restrict__ flag, const StencilArgs& a, int img, int by, int bx) {
     const int M = a.M, N = a.N;
     const size_t plane = (size_t)M * N;
-    const int img = blockIdx.z;
     const float* ph = phi + img * plane;
     const float* w1 = w_in + img * 2 * plane;
     const float* w2 = w1 + plane;
@@ -343,12 +429,12 @@ __global__ void __launch_bounds__(32 * ST_BY) k_wb(const float* __restrict__ phi
     float* b1 = bv + img * 2 * plane;
     float* b2 = b1 + plane;
     const float* gg = g + img * plane;
-    const int row0 = blockIdx.y * ST_TH, col0 = blockIdx.x * ST_TW;
-    stage_u<R>(U, ph, w1, w2, M, N, row0, col0, a.reg);
+    const int row0 = by * ST_TH, col0 = bx * ST_TW;
+    stage_u<R, LEQ>(U, ph, w1, w2, M, N, row0, col0, a.reg);
     __syncthreads();
     const int r0 = threadIdx.y * ST_RT, c0 = threadIdx.x * ST_CT;
     const int gj = col0 + c0;
-    if (gj >= N) return;
+    if (gj >= N || row0 + r0 >= M) return;
     float2 v[ST_RT][ST_CT];
     window_block<R, SHAPE>(U, r0, c0, a.e, v);
     bool bad = false;
@@ -377,7 +463,7 @@ __global__ void __launch_bounds__(32 * ST_BY) k_wb(const float* __restrict__ phi
             const float gp1 = (gi < M - 1) ? pn_[c] - ps : 0.f;
             const float gp2 = (j < N - 1) ? p_[c + 1] - ps : 0.f;
             float x, y, hh, dd;
-            reg_hd(ps, a.reg, hh, dd);
+            reg_hd<LEQ>(ps, a.reg, hh, dd);
             if (MODE == 0) {
                 const float Bx = gp1 + b1_[c] + a.beta2_mu * hh * v[i][c].x;
                 const float By = gp2 + b2_[c] + a.beta2_mu * hh * v[i][c].y;
@@ -415,6 +501,25 @@ __global__ void __launch_bounds__(32 * ST_BY) k_wb(const float* __restrict__ phi
         }
     }
     if (UPDATE_B && bad) atomicOr(flag, 1);
+}
+
+// One CTA per tile (grid = tiles_x x tiles_y x batch).  A persistent variant with one-tile-ahead L2
+// bulk prefetch (prefetch_tile) measured slower: the loop raised register pressure.
+template <int R, int SHAPE, bool LEQ>
+__global__ void __launch_bounds__(32 * ST_BY) k_rhs(const float* __restrict__ phi, const float* __restrict__ w,
+                                                    const float* __restrict__ bv, const float* __restrict__ g,
+                                                    float* __restrict__ D, StencilArgs a) {
+    extern __shared__ float4 U[];
+    rhs_tile<R, SHAPE, LEQ>(U, phi, w, bv, g, D, a, blockIdx.z, blockIdx.y, blockIdx.x);
+}
+
+template <int R, int SHAPE, int MODE, bool UPDATE_B, bool LEQ>
+__global__ void __launch_bounds__(32 * ST_BY) k_wb(const float* __restrict__ phi, const float* __restrict__ w_in,
+                                                   float* __restrict__ w_out, float* __restrict__ bv,
+                                                   const float* __restrict__ g, int* __restrict__ flag,
+                                                   StencilArgs a) {
+    extern __shared__ float4 U[];
+    wb_tile<R, SHAPE, MODE, UPDATE_B, LEQ>(U, phi, w_in, w_out, bv, g, flag, a, blockIdx.z, blockIdx.y, blockIdx.x);
 }
 
 }  // namespace srsb

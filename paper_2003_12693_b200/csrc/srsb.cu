@@ -149,11 +149,13 @@ sr_status configure(sr_sb_ctx* c) {
     c->csmem = G * 2 * c->ca.SC * (int)sizeof(float);
     // stencils
     int smem = 0;
-    bool ok = pick_stencil(p.window, p.window_shape, c->rhs, c->wb, smem);
+    bool ok = pick_stencil(p.window, p.window_shape, p.l == p.epsilon, c->rhs, c->wb, smem);
     if (!ok) return fail(c, SR_ERR_ARG, "window radius not supported");
     c->ssmem = smem;
-    c->sgrid = dim3((N + ST_TW - 1) / ST_TW, (M + ST_TH - 1) / ST_TH, B);
     c->sblock = dim3(32, ST_BY, 1);
+    c->sa.tiles_x = (N + ST_TW - 1) / ST_TW;
+    c->sa.tiles_y = (M + ST_TH - 1) / ST_TH;
+    c->sa.ntiles = c->sa.tiles_x * c->sa.tiles_y * B;
     StencilArgs& a = c->sa;
     a.M = M;
     a.N = N;
@@ -162,6 +164,7 @@ sr_status configure(sr_sb_ctx* c) {
     a.reg.l = p.l;
     a.reg.sl = (float)std::sin(3.14159265358979323846 * (double)p.l / (double)p.epsilon);
     a.reg.cl = (float)std::cos(3.14159265358979323846 * (double)p.l / (double)p.epsilon);
+    a.reg.l_eq_eps = (p.l == p.epsilon) ? 1 : 0;
     for (int q = 0; q <= 8; q++) a.e[q] = (float)std::exp(-(double)(q * q) / ((double)p.d * p.d));
     a.tau = p.tau;
     a.gamma = p.gamma;
@@ -180,6 +183,7 @@ sr_status configure(sr_sb_ctx* c) {
     for (int m = 0; m < 2; m++)
         for (int u = 0; u < 2; u++)
             CK(cudaFuncSetAttribute((const void*)c->wb[m][u], cudaFuncAttributeMaxDynamicSharedMemorySize, c->ssmem));
+    c->sgrid = dim3(c->sa.tiles_x, c->sa.tiles_y, B);
     return SR_OK;
 }
 

@@ -23,7 +23,9 @@
 
 namespace srsb {
 
-__device__ __forceinline__ int pad32(int i) { return i + (i >> 5); }
+// float2 shared-memory index with one pad slot per 16 complex values (128 B): strided butterfly
+// accesses with power-of-two strides <= 16 hit 16 distinct 8-byte bank pairs per half-warp.
+__device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
 
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
     return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
@@ -82,10 +84,9 @@ __device__ __forceinline__ void dft_reg(float2 (&x)[R]) {
 
 // Stockham stages of an N-point FFT (N = 2^LOGN) by T = N/E threads, thread t.
 // On entry of the first stage v[u] = x[t + u T]; on exit v[u] = X[t + u T].
-// sre/sim: this transform's padded SoA shared-memory row.  tw[m] = exp(-2 pi i m / N).
+// sm: this transform's padded float2 shared-memory row.  tw[m] = exp(-2 pi i m / N).
 template <int LOGN, int LOGE, int LOGNS, bool INV>
-__device__ __forceinline__ void fft_stages(float2 (&v)[1 << LOGE], float* __restrict__ sre,
-                                           float* __restrict__ sim, int t,
+__device__ __forceinline__ void fft_stages(float2 (&v)[1 << LOGE], float2* __restrict__ sm, int t,
                                            const float2* __restrict__ tw) {
     constexpr int N = 1 << LOGN, E = 1 << LOGE, T = N / E;
     constexpr int LOGR = (LOGN - LOGNS < LOGE) ? (LOGN - LOGNS) : LOGE;
@@ -95,10 +96,7 @@ __device__ __forceinline__ void fft_stages(float2 (&v)[1 << LOGE], float* __rest
 #pragma unroll
         for (int q = 0; q < Q; q++)
 #pragma unroll
-            for (int r = 0; r < R; r++) {
-                const int idx = pad32(t + q * T + r * (N / R));
-                v[q + r * Q] = make_float2(sre[idx], sim[idx]);
-            }
+            for (int r = 0; r < R; r++) v[q + r * Q] = sm[pad16(t + q * T + r * (N / R))];
         __syncthreads();
     }
 #pragma unroll
@@ -136,16 +134,12 @@ __device__ __forceinline__ void fft_stages(float2 (&v)[1 << LOGE], float* __rest
         } else {
             const int base = (j >> LOGNS) * (NS * R) + k;
 #pragma unroll
-            for (int r = 0; r < R; r++) {
-                const int idx = pad32(base + r * NS);
-                sre[idx] = x[r].x;
-                sim[idx] = x[r].y;
-            }
+            for (int r = 0; r < R; r++) sm[pad16(base + r * NS)] = x[r];
         }
     }
     if constexpr (!LAST) {
         __syncthreads();
-        fft_stages<LOGN, LOGE, LOGNS + LOGR, INV>(v, sre, sim, t, tw);
+        fft_stages<LOGN, LOGE, LOGNS + LOGR, INV>(v, sm, t, tw);
     }
 }
 
@@ -153,7 +147,7 @@ struct FftRowArgs {
     int M;          // rows per image
     int lg_rpc;     // log2 rows per CTA
     int lg_G;       // log2 column-group interleave of the spectrum
-    int SR;         // floats per shared row (re or im), padded
+    int SR;         // float2 per shared row, padded
     float clip;     // c2r only: > 0 clamps the output to [-clip, clip]
     int accum;      // c2r only: 1 -> phi = phi + z (increment form), 0 -> phi = z
 };
@@ -164,37 +158,31 @@ __global__ void __launch_bounds__(512) k_rows_r2c(const float* __restrict__ F, f
                                                    const float2* __restrict__ twH,
                                                    const float2* __restrict__ twR, FftRowArgs a) {
     constexpr int H = 1 << LOGH, E = 1 << LOGE, T = H / E;
-    extern __shared__ float smem[];
+    extern __shared__ float2 smem2[];
     const int tid = threadIdx.x;
     const int grp = tid / T, t = tid % T;
     const int rpc = 1 << a.lg_rpc, G = 1 << a.lg_G;
     const int b = blockIdx.y, m0 = blockIdx.x * rpc;
-    float* sre = smem + grp * 2 * a.SR;
-    float* sim = sre + a.SR;
+    float2* sm = smem2 + grp * a.SR;
     const float2* x = reinterpret_cast<const float2*>(F + ((size_t)b * a.M + m0 + grp) * (2 * H));
     float2 v[E];
 #pragma unroll
     for (int u = 0; u < E; u++) v[u] = __ldcs(x + t + u * T);
-    fft_stages<LOGH, LOGE, 0, false>(v, sre, sim, t, twH);
+    fft_stages<LOGH, LOGE, 0, false>(v, sm, t, twH);
+#pragma unroll
+    for (int u = 0; u < E; u++) sm[pad16(t + u * T)] = v[u];
+    __syncthreads();
+    float2* out = spec + (size_t)b * H * a.M;
 #pragma unroll
     for (int u = 0; u < E; u++) {
-        const int idx = pad32(t + u * T);
-        sre[idx] = v[u].x;
-        sim[idx] = v[u].y;
-    }
-    __syncthreads();
-    const int total = rpc * H;
-    float2* out = spec + (size_t)b * H * a.M;
-    for (int e = tid; e < total; e += blockDim.x) {
+        const int e = tid + u * blockDim.x;   // blockDim = rpc * T: exactly E elements per thread
         const int kk = e & (G - 1);
         const int rr = (e >> a.lg_G) & (rpc - 1);
         const int kg = e >> (a.lg_G + a.lg_rpc);
         const int k2 = (kg << a.lg_G) + kk;
-        const float* rre = smem + rr * 2 * a.SR;
-        const float* rim = rre + a.SR;
-        const float2 Zk = make_float2(rre[pad32(k2)], rim[pad32(k2)]);
-        const int kc = (H - k2) & (H - 1);
-        const float2 Zc = make_float2(rre[pad32(kc)], -rim[pad32(kc)]);
+        const float2* row = smem2 + rr * a.SR;
+        const float2 Zk = row[pad16(k2)];
+        const float2 Zc = conjf2(row[pad16((H - k2) & (H - 1))]);
         float2 X;
         if (k2 == 0) {
             X = make_float2(Zk.x + Zk.y, Zk.x - Zk.y);  // (X[0], X[N/2]) packed
@@ -211,47 +199,44 @@ __global__ void __launch_bounds__(512) k_rows_r2c(const float* __restrict__ F, f
 
 struct FftColArgs {
     int H;          // N/2: spectrum columns
-    int lg_G;       // columns per CTA (= layout interleave)
-    int SC;         // floats per shared row, padded
+    int lg_G;       // layout interleave (columns per group)
+    int lg_cpc;     // columns per CTA (a multiple of G)
+    int SC;         // float2 per shared row, padded
     float taumu;    // tau * mu
     float scale;    // 1 / (M H)
 };
 
-// Column pass: forward FFT, divide by the symbol, inverse FFT, in place.
+// Column pass: forward FFT, divide by the symbol, inverse FFT, in place.  Threads of one column
+// are consecutive (t fastest), so a warp works inside one transform.
 template <int LOGM, int LOGE>
 __global__ void __launch_bounds__(512) k_cols_solve(float2* __restrict__ spec, const float2* __restrict__ twM,
-                                                     const float* __restrict__ cM, const float* __restrict__ cN,
-                                                     FftColArgs a) {
+                                                       const float* __restrict__ cM, const float* __restrict__ cN,
+                                                       FftColArgs a) {
     constexpr int M = 1 << LOGM, E = 1 << LOGE, T = M / E;
-    extern __shared__ float smem[];
+    extern __shared__ float2 smem2[];
     const int G = 1 << a.lg_G;
     const int tid = threadIdx.x;
-    const int cc = tid & (G - 1), t = tid >> a.lg_G;
-    const int kg = blockIdx.x, b = blockIdx.y;
-    const int k2 = (kg << a.lg_G) + cc;
-    float2* base = spec + (size_t)b * a.H * M + (size_t)kg * M * G;
-    float* sre = smem + cc * 2 * a.SC;
-    float* sim = sre + a.SC;
+    const int t = tid % T, cl = tid / T;                 // cl: column within the CTA
+    const int k2 = (blockIdx.x << a.lg_cpc) + cl;         // spectrum column
+    const int b = blockIdx.y;
+    const int kg = k2 >> a.lg_G, cc = k2 & (G - 1);
+    float2* base = spec + (size_t)b * a.H * M + (size_t)kg * M * G + cc;
+    float2* sm = smem2 + cl * a.SC;
     float2 v[E];
 #pragma unroll
-    for (int u = 0; u < E; u++) v[u] = base[((t + u * T) << a.lg_G) + cc];
-    fft_stages<LOGM, LOGE, 0, false>(v, sre, sim, t, twM);
-    if (kg == 0) {  // CTA-uniform branch: slot 0 packs the real columns k2 = 0 and k2 = N/2
+    for (int u = 0; u < E; u++) v[u] = base[(size_t)(t + u * T) << a.lg_G];
+    fft_stages<LOGM, LOGE, 0, false>(v, sm, t, twM);
+    if (blockIdx.x == 0) {  // CTA-uniform branch: slot 0 packs the real columns k2 = 0 and k2 = N/2
 #pragma unroll
-        for (int u = 0; u < E; u++) {
-            const int idx = pad32(t + u * T);
-            sre[idx] = v[u].x;
-            sim[idx] = v[u].y;
-        }
+        for (int u = 0; u < E; u++) sm[pad16(t + u * T)] = v[u];
         __syncthreads();
-        if (cc == 0) {
+        if (k2 == 0) {
             const float c0 = __ldg(&cN[0]), ch = __ldg(&cN[a.H]);
 #pragma unroll
             for (int u = 0; u < E; u++) {
                 const int k1 = t + u * T;
-                const int kc = (M - k1) & (M - 1);
                 const float2 C = v[u];
-                const float2 Cc = make_float2(sre[pad32(kc)], -sim[pad32(kc)]);
+                const float2 Cc = conjf2(sm[pad16((M - k1) & (M - 1))]);
                 const float cm = __ldg(&cM[k1]);
                 const float s0 = a.scale / (1.f + a.taumu * (cm + c0));
                 const float sh = a.scale / (1.f + a.taumu * (cm + ch));
@@ -275,48 +260,60 @@ __global__ void __launch_bounds__(512) k_cols_solve(float2* __restrict__ spec, c
             v[u] = make_float2(v[u].x * s, v[u].y * s);
         }
     }
-    fft_stages<LOGM, LOGE, 0, true>(v, sre, sim, t, twM);
+    fft_stages<LOGM, LOGE, 0, true>(v, sm, t, twM);
 #pragma unroll
-    for (int u = 0; u < E; u++) base[((t + u * T) << a.lg_G) + cc] = v[u];
+    for (int u = 0; u < E; u++) base[(size_t)(t + u * T) << a.lg_G] = v[u];
 }
 
-// Row pass 2: transposed half spectrum -> inverse real FFT -> phi rows (optionally clamped).
+// Row pass 2: transposed half spectrum -> inverse real FFT -> phi rows (accumulated, clamped).
 template <int LOGH, int LOGE>
 __global__ void __launch_bounds__(512) k_rows_c2r(const float2* __restrict__ spec, float* __restrict__ phi,
                                                    const float2* __restrict__ twH,
                                                    const float2* __restrict__ twR, FftRowArgs a) {
     constexpr int H = 1 << LOGH, E = 1 << LOGE, T = H / E;
-    extern __shared__ float smem[];
+    extern __shared__ float2 smem2[];
     const int tid = threadIdx.x;
     const int grp = tid / T, t = tid % T;
     const int rpc = 1 << a.lg_rpc, G = 1 << a.lg_G;
     const int b = blockIdx.y, m0 = blockIdx.x * rpc;
     const float2* in = spec + (size_t)b * H * a.M;
-    const int total = rpc * H;
-    for (int e = tid; e < total; e += blockDim.x) {
-        const int kk = e & (G - 1);
-        const int rr = (e >> a.lg_G) & (rpc - 1);
-        const int kg = e >> (a.lg_G + a.lg_rpc);
-        const int k2 = (kg << a.lg_G) + kk;
-        const float2 X = in[(((size_t)kg * a.M + m0 + rr) << a.lg_G) + kk];
-        float* rre = smem + rr * 2 * a.SR;
-        rre[pad32(k2)] = X.x;
-        rre[a.SR + pad32(k2)] = X.y;
+    float2* out = reinterpret_cast<float2*>(phi + ((size_t)b * a.M + m0 + grp) * (2 * H));
+    // accumulation source (phi of the previous sweep), fetched first: its latency hides behind the FFT
+    float2 old[E];
+    if (a.accum) {
+#pragma unroll
+        for (int u = 0; u < E; u++) old[u] = out[t + u * T];
+    }
+    // transposed gather: blockDim = rpc * T threads, rpc * H elements -> exactly E per thread;
+    // all E loads are issued before the shared stores
+    {
+        float2 tmp[E];
+        int sidx[E];
+#pragma unroll
+        for (int u = 0; u < E; u++) {
+            const int e = tid + u * blockDim.x;
+            const int kk = e & (G - 1);
+            const int rr = (e >> a.lg_G) & (rpc - 1);
+            const int kg = e >> (a.lg_G + a.lg_rpc);
+            const int k2 = (kg << a.lg_G) + kk;
+            tmp[u] = __ldcs(in + (((size_t)kg * a.M + m0 + rr) << a.lg_G) + kk);
+            sidx[u] = rr * a.SR + pad16(k2);
+        }
+#pragma unroll
+        for (int u = 0; u < E; u++) smem2[sidx[u]] = tmp[u];
     }
     __syncthreads();
-    float* sre = smem + grp * 2 * a.SR;
-    float* sim = sre + a.SR;
+    float2* sm = smem2 + grp * a.SR;
     float2 v[E];
 #pragma unroll
     for (int u = 0; u < E; u++) {
         const int k = t + u * T;
-        const float2 X = make_float2(sre[pad32(k)], sim[pad32(k)]);
+        const float2 X = sm[pad16(k)];
         if (k == 0) {
             // X.x = X[0], X.y = X[N/2]: Z[0] = E[0] + i O[0], E = (X0 + Xh)/2, O = (X0 - Xh)/2
             v[u] = make_float2(0.5f * (X.x + X.y), 0.5f * (X.x - X.y));
         } else {
-            const int kc = H - k;
-            const float2 Xc = make_float2(sre[pad32(kc)], -sim[pad32(kc)]);
+            const float2 Xc = conjf2(sm[pad16(H - k)]);
             const float2 Ev = make_float2(0.5f * (X.x + Xc.x), 0.5f * (X.y + Xc.y));
             const float2 D = make_float2(0.5f * (X.x - Xc.x), 0.5f * (X.y - Xc.y));
             const float2 O = cmul(conjf2(__ldg(&twR[k])), D);  // W^{-k} D
@@ -324,15 +321,13 @@ __global__ void __launch_bounds__(512) k_rows_c2r(const float2* __restrict__ spe
         }
     }
     __syncthreads();
-    fft_stages<LOGH, LOGE, 0, true>(v, sre, sim, t, twH);
-    float2* out = reinterpret_cast<float2*>(phi + ((size_t)b * a.M + m0 + grp) * (2 * H));
+    fft_stages<LOGH, LOGE, 0, true>(v, sm, t, twH);
 #pragma unroll
     for (int u = 0; u < E; u++) {
         float2 z = v[u];
         if (a.accum) {
-            const float2 old = out[t + u * T];
-            z.x += old.x;
-            z.y += old.y;
+            z.x += old[u].x;
+            z.y += old[u].y;
         }
         if (a.clip > 0.f) {
             z.x = fminf(fmaxf(z.x, -a.clip), a.clip);

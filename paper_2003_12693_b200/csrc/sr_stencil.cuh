@@ -176,9 +176,9 @@ struct StencilArgs {
     int tiles_x, tiles_y, ntiles;   // persistent tile loop: tiles per row, per column, total (x batch)
 };
 
-constexpr int ST_CT = 4;   // columns per thread
+constexpr int ST_CT = 2;   // columns per thread
 constexpr int ST_RT = 8;   // rows per thread
-constexpr int ST_BY = 4;   // thread rows per CTA
+constexpr int ST_BY = 8;   // thread rows per CTA
 constexpr int ST_TW = 32 * ST_CT;
 constexpr int ST_TH = ST_BY * ST_RT;
 
@@ -191,6 +191,45 @@ struct TileGeom {
     static constexpr int ROWS = ST_TH + 2 * R;
     static constexpr int BYTES = LDC * ROWS * 16;
 };
+
+// CT-wide vector loads / stores (CT = 2: float2, CT = 4: float4); p must be CT*4-byte aligned.
+template <int CT>
+__device__ __forceinline__ void ldv(const float* __restrict__ p, float (&o)[CT]) {
+    if constexpr (CT == 4) {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(p));
+        o[0] = q.x; o[1] = q.y; o[2] = q.z; o[3] = q.w;
+    } else if constexpr (CT == 2) {
+        const float2 q = __ldg(reinterpret_cast<const float2*>(p));
+        o[0] = q.x; o[1] = q.y;
+    } else {
+#pragma unroll
+        for (int c = 0; c < CT; c++) o[c] = __ldg(p + c);
+    }
+}
+template <int CT>
+__device__ __forceinline__ void ldv_rw(const float* p, float (&o)[CT]) {   // coherent load (in-place fields)
+    if constexpr (CT == 4) {
+        const float4 q = *reinterpret_cast<const float4*>(p);
+        o[0] = q.x; o[1] = q.y; o[2] = q.z; o[3] = q.w;
+    } else if constexpr (CT == 2) {
+        const float2 q = *reinterpret_cast<const float2*>(p);
+        o[0] = q.x; o[1] = q.y;
+    } else {
+#pragma unroll
+        for (int c = 0; c < CT; c++) o[c] = p[c];
+    }
+}
+template <int CT>
+__device__ __forceinline__ void stv(float* p, const float (&o)[CT]) {
+    if constexpr (CT == 4) {
+        *reinterpret_cast<float4*>(p) = make_float4(o[0], o[1], o[2], o[3]);
+    } else if constexpr (CT == 2) {
+        *reinterpret_cast<float2*>(p) = make_float2(o[0], o[1]);
+    } else {
+#pragma unroll
+        for (int c = 0; c < CT; c++) p[c] = o[c];
+    }
+}
 
 // bank-conflict-free chunk swizzle: 8 consecutive even (or odd) chunks map to 8 distinct bank quads
 __device__ __forceinline__ int swz(int c) { return c ^ ((c >> 3) & 1); }
@@ -335,46 +374,41 @@ __device__ __forceinline__ void rhs_tile(float4* __restrict__ U, const float* __
     float2 v[ST_RT][ST_CT];
     window_block<R, SHAPE>(U, r0, c0, a.e, v);
     const int jl = (gj - 1) & (N - 1), jr = (gj + ST_CT) & (N - 1);   // periodic neighbours
+    constexpr int CT = ST_CT;
     // c1 = (b1 - w1) and psi of the row above the first output row
-    float c1p[ST_CT];
-    float4 Pu;
+    float c1p[CT], Pu[CT], P[CT];
     {
         const int gi = row0 + r0 - 1;
 #pragma unroll
-        for (int c = 0; c < ST_CT; c++) c1p[c] = 0.f;
+        for (int c = 0; c < CT; c++) c1p[c] = 0.f;
         if (gi >= 0) {
-            const float4 bb = __ldg(reinterpret_cast<const float4*>(b1 + (size_t)gi * N + gj));
-            const float4 ww = __ldg(reinterpret_cast<const float4*>(w1 + (size_t)gi * N + gj));
-            c1p[0] = bb.x - ww.x; c1p[1] = bb.y - ww.y; c1p[2] = bb.z - ww.z; c1p[3] = bb.w - ww.w;
+            float bb[CT], ww[CT];
+            ldv<CT>(b1 + (size_t)gi * N + gj, bb);
+            ldv<CT>(w1 + (size_t)gi * N + gj, ww);
+#pragma unroll
+            for (int c = 0; c < CT; c++) c1p[c] = bb[c] - ww[c];
         }
-        Pu = __ldg(reinterpret_cast<const float4*>(ph + (size_t)((gi + M) & (M - 1)) * N + gj));
+        ldv<CT>(ph + (size_t)((gi + M) & (M - 1)) * N + gj, Pu);
     }
-    float4 P4 = __ldg(reinterpret_cast<const float4*>(ph + (size_t)(row0 + r0) * N + gj));
+    ldv<CT>(ph + (size_t)(row0 + r0) * N + gj, P);
 #pragma unroll
     for (int i = 0; i < ST_RT; i++) {
         const int gi = row0 + r0 + i;
         if (gi >= M) break;
         const size_t o = (size_t)gi * N + gj;
-        const float4 Pd = __ldg(reinterpret_cast<const float4*>(ph + (size_t)((gi + 1) & (M - 1)) * N + gj));
+        float Pd[CT], w1_[CT], w2_[CT], b1_[CT], b2_[CT], g_[CT];
+        ldv<CT>(ph + (size_t)((gi + 1) & (M - 1)) * N + gj, Pd);
         const float pl = __ldg(ph + (size_t)gi * N + jl), pr = __ldg(ph + (size_t)gi * N + jr);
-        const float4 W1 = __ldg(reinterpret_cast<const float4*>(w1 + o));
-        const float4 W2 = __ldg(reinterpret_cast<const float4*>(w2 + o));
-        const float4 B1 = __ldg(reinterpret_cast<const float4*>(b1 + o));
-        const float4 B2 = __ldg(reinterpret_cast<const float4*>(b2 + o));
-        const float4 G4 = __ldg(reinterpret_cast<const float4*>(gg + o));
-        const float p_[6] = {pl, P4.x, P4.y, P4.z, P4.w, pr};
-        const float pu_[4] = {Pu.x, Pu.y, Pu.z, Pu.w};
-        const float pd_[4] = {Pd.x, Pd.y, Pd.z, Pd.w};
-        const float w1_[4] = {W1.x, W1.y, W1.z, W1.w};
-        const float w2_[4] = {W2.x, W2.y, W2.z, W2.w};
-        const float b1_[4] = {B1.x, B1.y, B1.z, B1.w};
-        const float b2_[4] = {B2.x, B2.y, B2.z, B2.w};
-        const float g_[4] = {G4.x, G4.y, G4.z, G4.w};
+        ldv<CT>(w1 + o, w1_);
+        ldv<CT>(w2 + o, w2_);
+        ldv<CT>(b1 + o, b1_);
+        ldv<CT>(b2 + o, b2_);
+        ldv<CT>(gg + o, g_);
         float c2l = 0.f;   // (b2 - w2) at column gj - 1 (non-periodic divergence, Eq. 36 / Q6)
         if (gj > 0) c2l = __ldg(b2 + o - 1) - __ldg(w2 + o - 1);
-        float out[4];
+        float out[CT];
 #pragma unroll
-        for (int c = 0; c < ST_CT; c++) {
+        for (int c = 0; c < CT; c++) {
             const int j = gj + c;
             const float c1 = b1_[c] - w1_[c];
             const float c2 = b2_[c] - w2_[c];
@@ -385,10 +419,12 @@ __device__ __forceinline__ void rhs_tile(float4* __restrict__ U, const float* __
             if (j > 0) dv -= c2l;
             c2l = c2;
             c1p[c] = c1;
-            const float ps = p_[c + 1];
+            const float ps = P[c];
+            const float left = c > 0 ? P[c > 0 ? c - 1 : 0] : pl;
+            const float right = c < CT - 1 ? P[c < CT - 1 ? c + 1 : 0] : pr;
             // neighbour differences first: exact (Sterbenz) for nearby values, so the O(1) level of
             // psi does not enter the rounding of the Laplacian
-            const float lap = ((pu_[c] - ps) + (pd_[c] - ps)) + ((p_[c] - ps) + (p_[c + 2] - ps));
+            const float lap = ((Pu[c] - ps) + (Pd[c] - ps)) + ((left - ps) + (right - ps));
             const float wn = sqrt_approx(w1_[c] * w1_[c] + w2_[c] * w2_[c]);
             const float wv = w1_[c] * v[i][c].x + w2_[c] * v[i][c].y;
             const RegVals rv = reg_all<LEQ>(ps, a.reg);
@@ -396,9 +432,12 @@ __device__ __forceinline__ void rhs_tile(float4* __restrict__ U, const float* __
                             a.mu * (dv + lap);
             out[c] = a.tau * t;
         }
-        *reinterpret_cast<float4*>(Do + o) = make_float4(out[0], out[1], out[2], out[3]);
-        Pu = P4;
-        P4 = Pd;
+        stv<CT>(Do + o, out);
+#pragma unroll
+        for (int c = 0; c < CT; c++) {
+            Pu[c] = P[c];
+            P[c] = Pd[c];
+        }
     }
 }
 
@@ -438,26 +477,31 @@ __device__ __forceinline__ void wb_tile(float4* __restrict__ U, const float* __r
     float2 v[ST_RT][ST_CT];
     window_block<R, SHAPE>(U, r0, c0, a.e, v);
     bool bad = false;
+    constexpr int CT = ST_CT;
 #pragma unroll
     for (int i = 0; i < ST_RT; i++) {
         const int gi = row0 + r0 + i;
         if (gi >= M) break;
         const size_t o = (size_t)gi * N + gj;
-        const float4 P4 = __ldg(reinterpret_cast<const float4*>(ph + o));
-        float4 Pn = P4;   // next row (grad component 1 is 0 on the last row)
-        if (gi < M - 1) Pn = __ldg(reinterpret_cast<const float4*>(ph + o + N));
-        const float pr = (gj + ST_CT < N) ? __ldg(ph + o + ST_CT) : 0.f;
-        const float4 B1 = *reinterpret_cast<const float4*>(b1 + o);
-        const float4 B2 = *reinterpret_cast<const float4*>(b2 + o);
-        const float4 G4 = __ldg(reinterpret_cast<const float4*>(gg + o));
-        const float p_[5] = {P4.x, P4.y, P4.z, P4.w, pr};
-        const float pn_[4] = {Pn.x, Pn.y, Pn.z, Pn.w};
-        const float b1_[4] = {B1.x, B1.y, B1.z, B1.w};
-        const float b2_[4] = {B2.x, B2.y, B2.z, B2.w};
-        const float g_[4] = {G4.x, G4.y, G4.z, G4.w};
-        float n1[4], n2[4], nb1[4], nb2[4];
+        float p_[CT + 1], pn_[CT], b1_[CT], b2_[CT], g_[CT];
+        {
+            float P[CT];
+            ldv<CT>(ph + o, P);
 #pragma unroll
-        for (int c = 0; c < ST_CT; c++) {
+            for (int c = 0; c < CT; c++) p_[c] = P[c];
+        }
+        if (gi < M - 1) ldv<CT>(ph + o + N, pn_);     // next row (grad component 1 is 0 on the last row)
+        else {
+#pragma unroll
+            for (int c = 0; c < CT; c++) pn_[c] = p_[c];
+        }
+        p_[CT] = (gj + CT < N) ? __ldg(ph + o + CT) : 0.f;
+        ldv_rw<CT>(b1 + o, b1_);
+        ldv_rw<CT>(b2 + o, b2_);
+        ldv<CT>(gg + o, g_);
+        float n1[CT], n2[CT], nb1[CT], nb2[CT];
+#pragma unroll
+        for (int c = 0; c < CT; c++) {
             const int j = gj + c;
             const float ps = p_[c];
             const float gp1 = (gi < M - 1) ? pn_[c] - ps : 0.f;
@@ -468,10 +512,10 @@ __device__ __forceinline__ void wb_tile(float4* __restrict__ U, const float* __r
                 const float Bx = gp1 + b1_[c] + a.beta2_mu * hh * v[i][c].x;
                 const float By = gp2 + b2_[c] + a.beta2_mu * hh * v[i][c].y;
                 const float t = a.gamma_mu * g_[c] * dd;
-                const float nb2 = Bx * Bx + By * By;
-                if (nb2 > 0.f) {
-                    const float inv = rsqrtf(nb2);           // 1/|B|
-                    const float m = fmaxf(1.f - t * inv, 0.f);  // max(|B| - t, 0)/|B|
+                const float nb2v = Bx * Bx + By * By;
+                if (nb2v > 0.f) {
+                    const float inv = rsqrtf(nb2v);              // 1/|B|
+                    const float m = fmaxf(1.f - t * inv, 0.f);   // max(|B| - t, 0)/|B|
                     x = m * Bx;
                     y = m * By;
                 } else {
@@ -493,11 +537,11 @@ __device__ __forceinline__ void wb_tile(float4* __restrict__ U, const float* __r
                 bad |= !isfinite(nb1[c]) || !isfinite(nb2[c]);
             }
         }
-        *reinterpret_cast<float4*>(o1 + o) = make_float4(n1[0], n1[1], n1[2], n1[3]);
-        *reinterpret_cast<float4*>(o2 + o) = make_float4(n2[0], n2[1], n2[2], n2[3]);
+        stv<CT>(o1 + o, n1);
+        stv<CT>(o2 + o, n2);
         if (UPDATE_B) {
-            *reinterpret_cast<float4*>(b1 + o) = make_float4(nb1[0], nb1[1], nb1[2], nb1[3]);
-            *reinterpret_cast<float4*>(b2 + o) = make_float4(nb2[0], nb2[1], nb2[2], nb2[3]);
+            stv<CT>(b1 + o, nb1);
+            stv<CT>(b2 + o, nb2);
         }
     }
     if (UPDATE_B && bad) atomicOr(flag, 1);

@@ -112,41 +112,46 @@ sr_status configure(sr_sb_ctx* c) {
     c->rinv = pick_row_inv(lgH);
     c->cols = pick_col(lgM);
     if (!c->rfwd || !c->rinv || !c->cols) return fail(c, SR_ERR_SHAPE, "no FFT kernel for this size");
-    // rows: rpc rows per CTA, E = min(16, H) values per thread
+    // rows: rpc rows per CTA (<= 512 threads, <= ~70 KB smem), E = min(16, H) values per thread
     const int E_h = H < 16 ? H : 16, T_h = H / E_h;
     int rpc = 8192 / H;
     if (rpc > 16) rpc = 16;
     if (rpc > M) rpc = M;
     if (rpc < 1) rpc = 1;
     while (rpc * T_h > 512) rpc >>= 1;
-    int G = 8192 / M;
-    if (G > 4) G = 4;
-    if (G > H) G = H;
+    // column-group interleave of the transposed spectrum: rpc * G >= 16 complex = 128 B stores
+    int G = 16 / rpc;
     if (G < 1) G = 1;
+    if (G > H) G = H;
     const int E_m = M < 16 ? M : 16, T_m = M / E_m;
-    while (G * T_m > 512) G >>= 1;
-    auto padded = [](int n, int extra) {
-        int sz = n + (n >> 5);
+    // columns per CTA: a multiple of G, <= 256 threads when possible (<= 512 always)
+    int cpc = G;
+    while (cpc * 2 * T_m <= 256 && cpc * 2 <= H) cpc *= 2;
+    while (cpc * T_m > 512 && cpc > G) cpc >>= 1;
+    if (cpc * T_m > 512) return fail(c, SR_ERR_SHAPE, "column FFT too large for one CTA");
+    auto padded = [](int n, int extra) {   // float2 slots: one pad per 16, rounded to 16, + extra
+        int sz = n + (n >> 4);
         sz = (sz + 15) & ~15;
         return sz + extra;
     };
     c->ra.M = M;
     c->ra.lg_rpc = ilog2(rpc);
     c->ra.lg_G = ilog2(G);
-    c->ra.SR = padded(H, G / 2 > 0 ? G / 2 : 1);
+    c->ra.SR = padded(H, G < 16 ? G : 1);
     c->ra.clip = 0.f;
     c->ra.accum = 0;
     c->rgrid = dim3(M / rpc, B, 1);
     c->rblock = dim3(rpc * T_h, 1, 1);
-    c->rsmem = rpc * 2 * c->ra.SR * (int)sizeof(float);
+    c->rsmem = rpc * c->ra.SR * (int)sizeof(float2);
     c->ca.H = H;
     c->ca.lg_G = ilog2(G);
+    c->ca.lg_cpc = ilog2(cpc);
     c->ca.SC = padded(M, 1);
     c->ca.taumu = p.tau * p.mu;
     c->ca.scale = (float)(1.0 / ((double)M * (double)H));
-    c->cgrid = dim3(H / G, B, 1);
-    c->cblock = dim3(G * T_m, 1, 1);
-    c->csmem = G * 2 * c->ca.SC * (int)sizeof(float);
+    c->cgrid = dim3(H / cpc, B, 1);
+    c->cblock = dim3(cpc * T_m, 1, 1);
+    c->csmem = cpc * c->ca.SC * (int)sizeof(float2);
     // stencils
     int smem = 0;
     bool ok = pick_stencil(p.window, p.window_shape, p.l == p.epsilon, c->rhs, c->wb, smem);

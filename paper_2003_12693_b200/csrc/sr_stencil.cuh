@@ -176,9 +176,16 @@ struct StencilArgs {
     int tiles_x, tiles_y, ntiles;   // persistent tile loop: tiles per row, per column, total (x batch)
 };
 
-constexpr int ST_CT = 2;   // columns per thread
-constexpr int ST_RT = 8;   // rows per thread
-constexpr int ST_BY = 8;   // thread rows per CTA
+#ifndef SRSB_ST_RT
+#define SRSB_ST_RT 8
+#endif
+#ifndef SRSB_ST_BY
+#define SRSB_ST_BY 8
+#endif
+constexpr int ST_CT = 2;            // columns per thread
+constexpr int ST_RT = SRSB_ST_RT;   // rows per thread
+constexpr int ST_BY = SRSB_ST_BY;   // thread rows per CTA
+constexpr int ST_MINB = 32 / ST_BY; // resident CTAs per SM the register budget targets (<= 64 regs)
 constexpr int ST_TW = 32 * ST_CT;
 constexpr int ST_TH = ST_BY * ST_RT;
 
@@ -550,7 +557,7 @@ __device__ __forceinline__ void wb_tile(float4* __restrict__ U, const float* __r
 // One CTA per tile (grid = tiles_x x tiles_y x batch).  A persistent variant with one-tile-ahead L2
 // bulk prefetch (prefetch_tile) measured slower: the loop raised register pressure.
 template <int R, int SHAPE, bool LEQ>
-__global__ void __launch_bounds__(32 * ST_BY) k_rhs(const float* __restrict__ phi, const float* __restrict__ w,
+__global__ void __launch_bounds__(32 * ST_BY, ST_MINB) k_rhs(const float* __restrict__ phi, const float* __restrict__ w,
                                                     const float* __restrict__ bv, const float* __restrict__ g,
                                                     float* __restrict__ D, StencilArgs a) {
     extern __shared__ float4 U[];
@@ -558,7 +565,7 @@ __global__ void __launch_bounds__(32 * ST_BY) k_rhs(const float* __restrict__ ph
 }
 
 template <int R, int SHAPE, int MODE, bool UPDATE_B, bool LEQ>
-__global__ void __launch_bounds__(32 * ST_BY) k_wb(const float* __restrict__ phi, const float* __restrict__ w_in,
+__global__ void __launch_bounds__(32 * ST_BY, ST_MINB) k_wb(const float* __restrict__ phi, const float* __restrict__ w_in,
                                                    float* __restrict__ w_out, float* __restrict__ bv,
                                                    const float* __restrict__ g, int* __restrict__ flag,
                                                    StencilArgs a) {

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsrsb.so")
+LIB_PATH = os.environ.get("SRSB_LIB", os.path.join(_HERE, "libsrsb.so"))
 
 SR_OK, SR_ERR_ARG, SR_ERR_SHAPE, SR_ERR_CUDA, SR_ERR_NONFINITE, SR_ERR_STATE, SR_ERR_OOM = 0, -1, -2, -3, -5, -6, -7
 STATUS_NAMES = {0: "SR_OK", -1: "SR_ERR_ARG", -2: "SR_ERR_SHAPE", -3: "SR_ERR_CUDA", -5: "SR_ERR_NONFINITE",

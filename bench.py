@@ -213,8 +213,9 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     B = cfg["batch"]
-    assert B % world == 0, "images must divide across ranks"
-    mine = list(range(rank * B // world, (rank + 1) * B // world))
+    from paper_2003_12693_b200.dist import max_over_ranks as _max_over_ranks, shard
+    s0, s1 = shard(B, world, rank)
+    mine = list(range(s0, s1))
     if args.config == "c3":
         data = make_config("c3", images=mine)
     else:
@@ -242,11 +243,7 @@ def main():
             torch.distributed.barrier()
 
     def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        return float(t.item())
+        return _max_over_ranks(x, device=dev)
 
     # ---------------------------------------------------------------- device-resident timing (value)
     with torch.cuda.stream(stream):

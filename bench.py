@@ -30,7 +30,7 @@ sys.path.insert(0, ROOT)
 METRIC = "megapixel-iterations/s per SB-SR iteration"
 UNIT = "Mpx-iter/s"
 # algorithmic HBM bytes per pixel per launch of each kernel class
-BYTES_PER_PX = {"rhs": 28.0, "rows_r2c": 8.0, "cols_solve": 8.0, "rows_c2r": 8.0, "wb": 40.0}
+BYTES_PER_PX = {"rhs": 28.0, "rows_r2c": 8.0, "cols_solve": 8.0, "rows_c2r": 12.0, "wb": 40.0}
 MODEL_BYTES_PER_PX_ITER = 172.0   # SURVEY.md §8(d) fused model (S = 3)
 
 

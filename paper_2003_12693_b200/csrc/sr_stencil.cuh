@@ -238,8 +238,9 @@ __device__ __forceinline__ void stv(float* p, const float (&o)[CT]) {
     }
 }
 
-// bank-conflict-free chunk swizzle: 8 consecutive even (or odd) chunks map to 8 distinct bank quads
-__device__ __forceinline__ int swz(int c) { return c ^ ((c >> 3) & 1); }
+// bank-conflict-free chunk swizzle for CT = 4 (stride-2 chunk reads): 8 consecutive even (or odd)
+// chunks map to 8 distinct bank quads.  CT = 2 reads consecutive chunks: identity.
+__device__ __forceinline__ int swz(int c) { return ST_CT == 4 ? c ^ ((c >> 3) & 1) : c; }
 
 // Stage u = h(phi) * w (two channels) over the tile + halo; zero outside the image (reading Q5).
 // One 2-pixel chunk per thread and step: float2 global loads, one float4 shared store.
@@ -349,6 +350,23 @@ __device__ __forceinline__ void prefetch_tile(const StencilArgs& a, int t, const
                           : f <= 4 ? bv + (2 * img + (f - 3)) * plane
                                    : g + img * plane;
         l2_prefetch(base + (size_t)r * N + c_lo, bytes);
+    }
+}
+
+// L2 bulk prefetch of the fields a warp reads only in its pointwise phase (b1, b2, g): issued at
+// tile start so their DRAM latency overlaps the staging and the window sum.
+__device__ __forceinline__ void prefetch_pointwise(const float* f0, const float* f1, const float* f2, int M, int N,
+                                                   int row0, int col0) {
+    const int lane = threadIdx.x;
+    const int r0 = threadIdx.y * ST_RT;
+    const int cols = min(ST_TW, N - col0);
+    for (int k = lane; k < ST_RT * 3; k += 32) {
+        const int i = k / 3, f = k - 3 * (k / 3);
+        const int gi = row0 + r0 + i;
+        if (gi < M) {
+            const float* base = f == 0 ? f0 : (f == 1 ? f1 : f2);
+            l2_prefetch(base + (size_t)gi * N + col0, (unsigned)cols * 4u);
+        }
     }
 }
 

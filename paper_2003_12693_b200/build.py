@@ -30,8 +30,11 @@ def _deps():
 def _compile(src: str, force: bool) -> tuple[str, str]:
     obj = os.path.join(OBJ, os.path.basename(src).replace(".cu", ".o"))
     log = obj + ".ptxas.log"
+    stamp = obj + ".flags"
+    flags = " ".join(ARCH + FLAGS)
     newest = max(os.path.getmtime(p) for p in [src] + _deps())
-    if not force and os.path.exists(obj) and os.path.getmtime(obj) >= newest:
+    same_flags = os.path.exists(stamp) and open(stamp).read() == flags
+    if not force and same_flags and os.path.exists(obj) and os.path.getmtime(obj) >= newest:
         return obj, "cached"
     cmd = [NVCC] + ARCH + FLAGS + ["-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -39,6 +42,8 @@ def _compile(src: str, force: bool) -> tuple[str, str]:
         f.write(r.stdout + r.stderr)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr[-4000:]}")
+    with open(stamp, "w") as f:
+        f.write(flags)
     return obj, "built"
 
 

@@ -123,7 +123,10 @@ sr_status configure(sr_sb_ctx* c) {
     int G = 16 / rpc;
     if (G < 1) G = 1;
     if (G > H) G = H;
-    const int E_m = M < 16 ? M : 16, T_m = M / E_m;
+#ifndef SRSB_COL_LOGE
+#define SRSB_COL_LOGE 4
+#endif
+    const int E_m = M < (1 << SRSB_COL_LOGE) ? M : (1 << SRSB_COL_LOGE), T_m = M / E_m;
     // columns per CTA: a multiple of G, <= 256 threads when possible (<= 512 always)
     int cpc = G;
     while (cpc * 2 * T_m <= 256 && cpc * 2 <= H) cpc *= 2;

@@ -1,10 +1,7 @@
 // Instantiations of the column solve pass (sr_fft.cuh) for M = 8 .. 8192.
 #include "sr_kernels.h"
 namespace srsb {
-#ifndef SRSB_COL_LOGE
-#define SRSB_COL_LOGE 4
-#endif
-template <int LG> static ColKernel cs() { return k_cols_solve<LG, (LG < SRSB_COL_LOGE ? LG : SRSB_COL_LOGE)>; }
+template <int LG> static ColKernel cs() { return k_cols_solve<LG, (LG < 4 ? LG : 4)>; }
 ColKernel pick_col(int lg) {
     switch (lg) {
         case 3: return cs<3>();   case 4: return cs<4>();   case 5: return cs<5>();   case 6: return cs<6>();

@@ -4,6 +4,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -112,25 +113,34 @@ sr_status configure(sr_sb_ctx* c) {
     c->rinv = pick_row_inv(lgH);
     c->cols = pick_col(lgM);
     if (!c->rfwd || !c->rinv || !c->cols) return fail(c, SR_ERR_SHAPE, "no FFT kernel for this size");
-    // rows: rpc rows per CTA (<= 512 threads, <= ~70 KB smem), E = min(16, H) values per thread
+    // Launch shapes (measured on B200, C3: smaller CTAs overlap load and FFT phases better):
+    //  rows: rpc rows per CTA, 64..512 threads, <= ~72 KB shared;  E = min(16, H) values per thread
     const int E_h = H < 16 ? H : 16, T_h = H / E_h;
-    int rpc = 8192 / H;
-    if (rpc > 16) rpc = 16;
+    int rpc = 8;
+    while (rpc * T_h < 64 && rpc < 32) rpc <<= 1;
+    while ((rpc * T_h > 512 || rpc * (H + H / 16 + 32) * 8 > 72 * 1024) && rpc > 1) rpc >>= 1;
     if (rpc > M) rpc = M;
-    if (rpc < 1) rpc = 1;
-    while (rpc * T_h > 512) rpc >>= 1;
-    // column-group interleave of the transposed spectrum: rpc * G >= 16 complex = 128 B stores
-    int G = 16 / rpc;
+    if (const char* ev = std::getenv("SRSB_RPC")) {   // tuning knob (power of two)
+        const int v = std::atoi(ev);
+        if (v >= 1 && v <= M && v * T_h <= 512 && (v & (v - 1)) == 0) rpc = v;
+    }
+    //  column-group interleave of the transposed spectrum: rpc * G >= 8 complex = 64 B contiguous
+    int G = 8 / rpc;
     if (G < 1) G = 1;
     if (G > H) G = H;
-#ifndef SRSB_COL_LOGE
-#define SRSB_COL_LOGE 4
-#endif
-    const int E_m = M < (1 << SRSB_COL_LOGE) ? M : (1 << SRSB_COL_LOGE), T_m = M / E_m;
-    // columns per CTA: a multiple of G, <= 256 threads when possible (<= 512 always)
+    if (const char* ev = std::getenv("SRSB_G")) {     // tuning knob (power of two)
+        const int v = std::atoi(ev);
+        if (v >= 1 && v <= H && (v & (v - 1)) == 0) G = v;
+    }
+    //  columns per CTA: a multiple of G, >= 64 threads, <= 512
+    const int E_m = M < 16 ? M : 16, T_m = M / E_m;
     int cpc = G;
-    while (cpc * 2 * T_m <= 256 && cpc * 2 <= H) cpc *= 2;
+    while (cpc * T_m < 64 && cpc * 2 <= H) cpc *= 2;
     while (cpc * T_m > 512 && cpc > G) cpc >>= 1;
+    if (const char* ev = std::getenv("SRSB_CPC")) {   // tuning knob (power of two, multiple of G)
+        const int v = std::atoi(ev);
+        if (v >= G && v <= H && v * T_m <= 512 && (v & (v - 1)) == 0) cpc = v;
+    }
     if (cpc * T_m > 512) return fail(c, SR_ERR_SHAPE, "column FFT too large for one CTA");
     auto padded = [](int n, int extra) {   // float2 slots: one pad per 16, rounded to 16, + extra
         int sz = n + (n >> 4);

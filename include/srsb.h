@@ -45,6 +45,7 @@ typedef enum {
     SR_ERR_ARG = -1,        /* invalid parameter or NULL pointer */
     SR_ERR_SHAPE = -2,      /* M, N not powers of two in [8, 8192], batch < 1 */
     SR_ERR_CUDA = -3,       /* CUDA runtime error; message in sr_sb_last_error */
+    SR_ERR_NCCL = -4,       /* NCCL error (slab mode); message in sr_sb_last_error */
     SR_ERR_NONFINITE = -5,  /* NaN/Inf or |b| > b_max latched by the w/b kernel */
     SR_ERR_STATE = -6,      /* call order violated (e.g. iterate before set_image) */
     SR_ERR_OOM = -7         /* device allocation failed */
@@ -81,8 +82,33 @@ void sr_sb_default_params(sr_sb_params* p, int M, int N, int batch, int window);
 
 /* Validate p, allocate all state on `device` (fields, spectrum, tables) and bind
  * the context to `stream` (a cudaStream_t; NULL = the legacy default stream).
- * Device memory: about 44 bytes per pixel. */
+ * Device memory: about 44 bytes per pixel plus 2 x max(window, ceil(3 sigma)+1) ghost rows per
+ * image plane. */
 sr_status sr_sb_create(const sr_sb_params* p, int device, void* stream, sr_sb_ctx** out);
+
+/* ---- Slab decomposition of ONE large image (batch must be 1) into P = nranks row slabs
+ * (BASELINE configs[4]).  Slab r holds global rows [r M/P, (r+1) M/P); the
+ * repulsion / divergence / gradient stencils read ghost rows filled by halo exchanges with the
+ * neighbouring slabs, the phi solve transposes the packed half spectrum with an all-to-all
+ * between its row pass and its column pass and back (Eq. 31-33 unchanged: the same butterflies
+ * as one GPU, so P slabs reproduce P = 1 bitwise).  Requirements: P a power of two,
+ * (N/2) % P == 0, M/P >= 8 and >= the ghost rows (max(window, ceil(3 sigma) + 1)).
+ *
+ * sr_sb_create_slab_group: all P slab contexts in this process on `device`, exchanges as device
+ *   copies (the single-GPU emulation of the multi-GPU schedule).  The returned handle presents
+ *   the FULL image: set_image / get_phi / get_state(phi, g) take [1][M][N] buffers; set_state,
+ *   profile and the debug entries are not available.
+ * sr_sb_create_slab_nccl: this process's slab `rank` of `nranks`, one process per GPU; halos by
+ *   ncclSend/ncclRecv, the transpose by ncclAlltoAll, on the context's stream (NVLink /
+ *   NVSwitch).  `nccl_id` = NCCL_UNIQUE_ID_BYTES (128) bytes from sr_sb_nccl_unique_id on one
+ *   rank, broadcast by the caller.  Buffers of set_image / get_phi / get_state are the LOCAL rows
+ *   [1][M/P][N] (sr_sb_local_rows). */
+sr_status sr_sb_create_slab_group(const sr_sb_params* p, int device, void* stream, int nslabs, sr_sb_ctx** out);
+sr_status sr_sb_nccl_unique_id(void* id_out, int bytes);
+sr_status sr_sb_create_slab_nccl(const sr_sb_params* p, int device, void* stream, int nranks, int rank,
+                                 const void* nccl_id, sr_sb_ctx** out);
+/* Rows per image held in the caller-visible buffers of this context (M, or M/P for an NCCL slab). */
+int sr_sb_local_rows(const sr_sb_ctx* ctx);
 
 /* Algorithm 1 step (1): image f and initial level set phi0 ([batch][M][N]) ->
  * g (Eq. 1), phi = phi0, w = grad phi0 (Q12), b = 0.  Resets k to 0. */

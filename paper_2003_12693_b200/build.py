@@ -18,8 +18,21 @@ LIB = os.path.join(HERE, "libsrsb.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-Xptxas", "-v",
-         "--expt-relaxed-constexpr"] + os.environ.get("SRSB_NVCC_FLAGS", "").split()
+def _nccl_dir():
+    """NCCL 2.28 shipped with the torch wheel (nvidia-nccl): headers + libnccl.so.2."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in (spec.submodule_search_locations if spec else []):
+        d = os.path.join(base, "nccl")
+        if os.path.exists(os.path.join(d, "include", "nccl.h")):
+            return d
+    raise RuntimeError("nccl.h not found (nvidia-nccl wheel)")
+
+
+NCCL = _nccl_dir()
+FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-I", INCLUDE, "-I", os.path.join(NCCL, "include"),
+         "-Xptxas", "-v", "--expt-relaxed-constexpr"] + os.environ.get("SRSB_NVCC_FLAGS", "").split()
+LDFLAGS = ["-L", os.path.join(NCCL, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(NCCL, "lib")]
 
 
 def _deps():
@@ -58,7 +71,7 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -
         os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs)
     if relink:
         tmp = LIB + ".tmp"
-        cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart"]
+        cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart"] + LDFLAGS
         subprocess.check_call(cmd)
         os.replace(tmp, LIB)
     if verbose:

@@ -144,7 +144,8 @@ __device__ __forceinline__ void fft_stages(float2 (&v)[1 << LOGE], float2* __res
 }
 
 struct FftRowArgs {
-    int M;          // rows per image
+    long long plane;  // elements per image plane of the real fields (ghost rows included)
+    int M;          // rows per image (local rows of the slab)
     int lg_rpc;     // log2 rows per CTA
     int lg_G;       // log2 column-group interleave of the spectrum
     int SR;         // float2 per shared row, padded
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(512) k_rows_r2c(const float* __restrict__ F, f
     const int rpc = 1 << a.lg_rpc, G = 1 << a.lg_G;
     const int b = blockIdx.y, m0 = blockIdx.x * rpc;
     float2* sm = smem2 + grp * a.SR;
-    const float2* x = reinterpret_cast<const float2*>(F + ((size_t)b * a.M + m0 + grp) * (2 * H));
+    const float2* x = reinterpret_cast<const float2*>(F + b * a.plane + (long long)(m0 + grp) * (2 * H));
     float2 v[E];
 #pragma unroll
     for (int u = 0; u < E; u++) v[u] = __ldcs(x + t + u * T);
@@ -197,13 +198,21 @@ __global__ void __launch_bounds__(512) k_rows_r2c(const float* __restrict__ F, f
     }
 }
 
+// Column element m of local spectrum column k2l (group kg = k2l / G, lane cc = k2l % G) lives at
+//   b * bstride + (m >> lg_seg) * seg_stride + ((kg * 2^lg_seg + m % 2^lg_seg) * G + cc)
+// i.e. the column is split into segments of 2^lg_seg rows (the slabs' row blocks after the
+// all-to-all; one segment = the whole column for a single-GPU image).
 struct FftColArgs {
-    int H;          // N/2: spectrum columns
+    int H;          // N/2: global spectrum columns (cN[H] is the k2 = N/2 symbol term)
     int lg_G;       // layout interleave (columns per group)
     int lg_cpc;     // columns per CTA (a multiple of G)
     int SC;         // float2 per shared row, padded
     float taumu;    // tau * mu
-    float scale;    // 1 / (M H)
+    float scale;    // 1 / (M H), global M
+    int lg_seg;     // log2 rows per segment (power of two)
+    long long seg_stride;  // complex elements between segments
+    long long bstride;     // complex elements between images
+    int k2_off;     // global index of local column 0 (slab: rank * H / P)
 };
 
 // Column pass: forward FFT, divide by the symbol, inverse FFT, in place.  Threads of one column
@@ -217,16 +226,24 @@ __global__ void __launch_bounds__(512) k_cols_solve(float2* __restrict__ spec, c
     const int G = 1 << a.lg_G;
     const int tid = threadIdx.x;
     const int t = tid % T, cl = tid / T;                 // cl: column within the CTA
-    const int k2 = (blockIdx.x << a.lg_cpc) + cl;         // spectrum column
+    const int k2l = (blockIdx.x << a.lg_cpc) + cl;        // local spectrum column
+    const int k2 = a.k2_off + k2l;                         // global spectrum column
     const int b = blockIdx.y;
-    const int kg = k2 >> a.lg_G, cc = k2 & (G - 1);
-    float2* base = spec + (size_t)b * a.H * M + (size_t)kg * M * G + cc;
+    const int kg = k2l >> a.lg_G, cc = k2l & (G - 1);
+    float2* base = spec + b * a.bstride + cc;
     float2* sm = smem2 + cl * a.SC;
+    long long addr[E];
+#pragma unroll
+    for (int u = 0; u < E; u++) {
+        const int m = t + u * T;
+        const int s = m >> a.lg_seg, mr = m & ((1 << a.lg_seg) - 1);
+        addr[u] = s * a.seg_stride + ((long long)((kg << a.lg_seg) + mr) << a.lg_G);
+    }
     float2 v[E];
 #pragma unroll
-    for (int u = 0; u < E; u++) v[u] = base[(size_t)(t + u * T) << a.lg_G];
+    for (int u = 0; u < E; u++) v[u] = base[addr[u]];
     fft_stages<LOGM, LOGE, 0, false>(v, sm, t, twM);
-    if (blockIdx.x == 0) {  // CTA-uniform branch: slot 0 packs the real columns k2 = 0 and k2 = N/2
+    if (blockIdx.x == 0 && a.k2_off == 0) {  // CTA-uniform: slot 0 packs the real columns k2 = 0, N/2
 #pragma unroll
         for (int u = 0; u < E; u++) sm[pad16(t + u * T)] = v[u];
         __syncthreads();
@@ -262,7 +279,7 @@ __global__ void __launch_bounds__(512) k_cols_solve(float2* __restrict__ spec, c
     }
     fft_stages<LOGM, LOGE, 0, true>(v, sm, t, twM);
 #pragma unroll
-    for (int u = 0; u < E; u++) base[(size_t)(t + u * T) << a.lg_G] = v[u];
+    for (int u = 0; u < E; u++) base[addr[u]] = v[u];
 }
 
 // Row pass 2: transposed half spectrum -> inverse real FFT -> phi rows (accumulated, clamped).
@@ -277,7 +294,7 @@ __global__ void __launch_bounds__(512) k_rows_c2r(const float2* __restrict__ spe
     const int rpc = 1 << a.lg_rpc, G = 1 << a.lg_G;
     const int b = blockIdx.y, m0 = blockIdx.x * rpc;
     const float2* in = spec + (size_t)b * H * a.M;
-    float2* out = reinterpret_cast<float2*>(phi + ((size_t)b * a.M + m0 + grp) * (2 * H));
+    float2* out = reinterpret_cast<float2*>(phi + b * a.plane + (long long)(m0 + grp) * (2 * H));
     // accumulation source (phi of the previous sweep), fetched first: its latency hides behind the FFT
     float2 old[E];
     if (a.accum) {

@@ -164,8 +164,15 @@ __host__ __device__ constexpr int half_width(int p) {
     return SHAPE == 0 ? isqrt_c(R * R - p * p) : R;
 }
 
+// Field layout (all kernels): pointers address local row 0 of image 0; image b, local row i
+// (-gh <= i < M + gh: gh ghost rows above and below, filled by the slab halo exchange) is at
+// p + b * plane + i * N.  M = local rows; Mg = global rows; row_off = global index of local row 0.
+// slab = 0: the whole image is local (M = Mg), periodic neighbours wrap in-kernel; slab = 1: the
+// neighbours of rows 0 and M-1 live in the ghost rows (the periodic wrap rows at ranks 0 and P-1).
 struct StencilArgs {
     int M, N;
+    int Mg, row_off, slab;
+    long long plane;
     Reg reg;
     float e[9];        // e_q = exp(-q^2/d^2), q = 0..8
     float tau, gamma, alpha, beta, mu;
@@ -247,7 +254,7 @@ __device__ __forceinline__ int swz(int c) { return ST_CT == 4 ? c ^ ((c >> 3) & 
 template <int R, bool LEQ>
 __device__ __forceinline__ void stage_u(float4* __restrict__ U, const float* __restrict__ phi,
                                         const float* __restrict__ w1, const float* __restrict__ w2,
-                                        int M, int N, int row0, int col0, const Reg& reg) {
+                                        int Mg, int row_off, int N, int row0, int col0, const Reg& reg) {
     using TG = TileGeom<R>;
     const int tid = threadIdx.y * 32 + threadIdx.x;
     constexpr int NTH = 32 * ST_BY;
@@ -257,8 +264,8 @@ __device__ __forceinline__ void stage_u(float4* __restrict__ U, const float* __r
         const int r = e / TG::CH, f = e - r * TG::CH;
         const int gi = row0 - R + r, gj = col0 - TG::RA + 2 * f;
         float4 A = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (gi >= 0 && gi < M && gj >= 0 && gj < N) {
-            const size_t o = (size_t)gi * N + gj;
+        if (gi + row_off >= 0 && gi + row_off < Mg && gj >= 0 && gj < N) {
+            const long long o = (long long)gi * N + gj;   // gi may address a ghost row
             const float2 P = __ldg(reinterpret_cast<const float2*>(phi + o));
             const float2 X = __ldg(reinterpret_cast<const float2*>(w1 + o));
             const float2 Y = __ldg(reinterpret_cast<const float2*>(w2 + o));
@@ -322,54 +329,6 @@ __device__ __forceinline__ void window_block(const float4* __restrict__ U, int r
     }
 }
 
-// Bulk L2 prefetch (cp.async.bulk.prefetch.L2) of the halo extent of one tile of `nf` fields:
-// rows [row0 - R, row0 + TH + R), columns [col0 - RA, col0 + TW + RA) clipped to the image, 16 B
-// aligned.  Issued one tile ahead by the persistent loop so the demand loads of the next tile hit L2.
-__device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-template <int R>
-__device__ __forceinline__ void prefetch_tile(const StencilArgs& a, int t, const float* phi, const float* w,
-                                              const float* bv, const float* g) {
-    using TG = TileGeom<R>;
-    const int M = a.M, N = a.N;
-    const int bx = t % a.tiles_x, rq = t / a.tiles_x;
-    const int by = rq % a.tiles_y, img = rq / a.tiles_y;
-    const int row0 = by * ST_TH, col0 = bx * ST_TW;
-    const size_t plane = (size_t)M * N;
-    const int tid = threadIdx.y * 32 + threadIdx.x;
-    const int r_lo = max(row0 - R - 1, 0), r_hi = min(row0 + ST_TH + R + 1, M);
-    const int c_lo = max(col0 - TG::RA, 0) & ~3, c_hi = (min(col0 + ST_TW + TG::RA, N) + 3) & ~3;
-    const unsigned bytes = (unsigned)(c_hi - c_lo) * 4u;
-    const int rows = r_hi - r_lo;
-    for (int e = tid; e < rows * 6; e += 32 * ST_BY) {
-        const int f = e / rows, r = r_lo + (e - f * rows);
-        // fields: phi, w1, w2, b1, b2, g of image img
-        const float* base = f == 0 ? phi + img * plane
-                          : f <= 2 ? w + (2 * img + (f - 1)) * plane
-                          : f <= 4 ? bv + (2 * img + (f - 3)) * plane
-                                   : g + img * plane;
-        l2_prefetch(base + (size_t)r * N + c_lo, bytes);
-    }
-}
-
-// L2 bulk prefetch of the fields a warp reads only in its pointwise phase (b1, b2, g): issued at
-// tile start so their DRAM latency overlaps the staging and the window sum.
-__device__ __forceinline__ void prefetch_pointwise(const float* f0, const float* f1, const float* f2, int M, int N,
-                                                   int row0, int col0) {
-    const int lane = threadIdx.x;
-    const int r0 = threadIdx.y * ST_RT;
-    const int cols = min(ST_TW, N - col0);
-    for (int k = lane; k < ST_RT * 3; k += 32) {
-        const int i = k / 3, f = k - 3 * (k / 3);
-        const int gi = row0 + r0 + i;
-        if (gi < M) {
-            const float* base = f == 0 ? f0 : (f == 1 ? f1 : f2);
-            l2_prefetch(base + (size_t)gi * N + col0, (unsigned)cols * 4u);
-        }
-    }
-}
-
 // Increment form of Eq. (37):  D = F - A psi, A = 1 - tau mu Delta_per, i.e.
 //   D = tau [ -gamma g |w| delta'(psi) + alpha g delta(psi) + 2 beta h'(psi) w.v + mu div(b - w)
 //             + mu Delta_per psi ],
@@ -382,7 +341,7 @@ __device__ __forceinline__ void rhs_tile(float4* __restrict__ U, const float* __
                                          const float* __restrict__ g, float* __restrict__ D, const StencilArgs& a,
                                          int img, int by, int bx) {
     const int M = a.M, N = a.N;
-    const size_t plane = (size_t)M * N;
+    const long long plane = a.plane;
     const float* ph = phi + img * plane;
     const float* w1 = w + img * 2 * plane;
     const float* w2 = w1 + plane;
@@ -391,7 +350,7 @@ __device__ __forceinline__ void rhs_tile(float4* __restrict__ U, const float* __
     const float* gg = g + img * plane;
     float* Do = D + img * plane;
     const int row0 = by * ST_TH, col0 = bx * ST_TW;
-    stage_u<R, LEQ>(U, ph, w1, w2, M, N, row0, col0, a.reg);
+    stage_u<R, LEQ>(U, ph, w1, w2, a.Mg, a.row_off, N, row0, col0, a.reg);
     __syncthreads();
     const int r0 = threadIdx.y * ST_RT, c0 = threadIdx.x * ST_CT;
     const int gj = col0 + c0;
@@ -400,30 +359,33 @@ __device__ __forceinline__ void rhs_tile(float4* __restrict__ U, const float* __
     window_block<R, SHAPE>(U, r0, c0, a.e, v);
     const int jl = (gj - 1) & (N - 1), jr = (gj + ST_CT) & (N - 1);   // periodic neighbours
     constexpr int CT = ST_CT;
+    // periodic row neighbour: wrapped in-kernel for a whole image, a ghost row in slab mode
+    auto prow = [&](int x) { return a.slab ? x : (x + M) & (M - 1); };
     // c1 = (b1 - w1) and psi of the row above the first output row
     float c1p[CT], Pu[CT], P[CT];
     {
         const int gi = row0 + r0 - 1;
 #pragma unroll
         for (int c = 0; c < CT; c++) c1p[c] = 0.f;
-        if (gi >= 0) {
+        if (gi + a.row_off >= 0) {
             float bb[CT], ww[CT];
-            ldv<CT>(b1 + (size_t)gi * N + gj, bb);
-            ldv<CT>(w1 + (size_t)gi * N + gj, ww);
+            ldv<CT>(b1 + (long long)gi * N + gj, bb);
+            ldv<CT>(w1 + (long long)gi * N + gj, ww);
 #pragma unroll
             for (int c = 0; c < CT; c++) c1p[c] = bb[c] - ww[c];
         }
-        ldv<CT>(ph + (size_t)((gi + M) & (M - 1)) * N + gj, Pu);
+        ldv<CT>(ph + (long long)prow(gi) * N + gj, Pu);
     }
-    ldv<CT>(ph + (size_t)(row0 + r0) * N + gj, P);
+    ldv<CT>(ph + (long long)(row0 + r0) * N + gj, P);
 #pragma unroll
     for (int i = 0; i < ST_RT; i++) {
         const int gi = row0 + r0 + i;
         if (gi >= M) break;
-        const size_t o = (size_t)gi * N + gj;
+        const int gig = gi + a.row_off;   // global row
+        const long long o = (long long)gi * N + gj;
         float Pd[CT], w1_[CT], w2_[CT], b1_[CT], b2_[CT], g_[CT];
-        ldv<CT>(ph + (size_t)((gi + 1) & (M - 1)) * N + gj, Pd);
-        const float pl = __ldg(ph + (size_t)gi * N + jl), pr = __ldg(ph + (size_t)gi * N + jr);
+        ldv<CT>(ph + (long long)prow(gi + 1) * N + gj, Pd);
+        const float pl = __ldg(ph + o - gj + jl), pr = __ldg(ph + o - gj + jr);
         ldv<CT>(w1 + o, w1_);
         ldv<CT>(w2 + o, w2_);
         ldv<CT>(b1 + o, b1_);
@@ -438,8 +400,8 @@ __device__ __forceinline__ void rhs_tile(float4* __restrict__ U, const float* __
             const float c1 = b1_[c] - w1_[c];
             const float c2 = b2_[c] - w2_[c];
             float dv = 0.f;
-            if (gi < M - 1) dv += c1;
-            if (gi > 0) dv -= c1p[c];
+            if (gig < a.Mg - 1) dv += c1;
+            if (gig > 0) dv -= c1p[c];
             if (j < N - 1) dv += c2;
             if (j > 0) dv -= c2l;
             c2l = c2;
@@ -484,7 +446,7 @@ __device__ __forceinline__ void wb_tile(float4* __restrict__ U, const float* __r
                                         float* __restrict__ bv, const float* __restrict__ g,
                                         int* __restrict__ flag, const StencilArgs& a, int img, int by, int bx) {
     const int M = a.M, N = a.N;
-    const size_t plane = (size_t)M * N;
+    const long long plane = a.plane;
     const float* ph = phi + img * plane;
     const float* w1 = w_in + img * 2 * plane;
     const float* w2 = w1 + plane;
@@ -494,7 +456,7 @@ __device__ __forceinline__ void wb_tile(float4* __restrict__ U, const float* __r
     float* b2 = b1 + plane;
     const float* gg = g + img * plane;
     const int row0 = by * ST_TH, col0 = bx * ST_TW;
-    stage_u<R, LEQ>(U, ph, w1, w2, M, N, row0, col0, a.reg);
+    stage_u<R, LEQ>(U, ph, w1, w2, a.Mg, a.row_off, N, row0, col0, a.reg);
     __syncthreads();
     const int r0 = threadIdx.y * ST_RT, c0 = threadIdx.x * ST_CT;
     const int gj = col0 + c0;
@@ -507,7 +469,8 @@ __device__ __forceinline__ void wb_tile(float4* __restrict__ U, const float* __r
     for (int i = 0; i < ST_RT; i++) {
         const int gi = row0 + r0 + i;
         if (gi >= M) break;
-        const size_t o = (size_t)gi * N + gj;
+        const int gig = gi + a.row_off;   // global row
+        const long long o = (long long)gi * N + gj;
         float p_[CT + 1], pn_[CT], b1_[CT], b2_[CT], g_[CT];
         {
             float P[CT];
@@ -515,7 +478,8 @@ __device__ __forceinline__ void wb_tile(float4* __restrict__ U, const float* __r
 #pragma unroll
             for (int c = 0; c < CT; c++) p_[c] = P[c];
         }
-        if (gi < M - 1) ldv<CT>(ph + o + N, pn_);     // next row (grad component 1 is 0 on the last row)
+        if (gig < a.Mg - 1) ldv<CT>(ph + o + N, pn_);   // next row (a ghost row at the slab edge;
+                                                         // grad component 1 is 0 on the last image row)
         else {
 #pragma unroll
             for (int c = 0; c < CT; c++) pn_[c] = p_[c];
@@ -529,7 +493,7 @@ __device__ __forceinline__ void wb_tile(float4* __restrict__ U, const float* __r
         for (int c = 0; c < CT; c++) {
             const int j = gj + c;
             const float ps = p_[c];
-            const float gp1 = (gi < M - 1) ? pn_[c] - ps : 0.f;
+            const float gp1 = (gig < a.Mg - 1) ? pn_[c] - ps : 0.f;
             const float gp2 = (j < N - 1) ? p_[c + 1] - ps : 0.f;
             float x, y, hh, dd;
             reg_hd<LEQ>(ps, a.reg, hh, dd);
@@ -573,7 +537,7 @@ __device__ __forceinline__ void wb_tile(float4* __restrict__ U, const float* __r
 }
 
 // One CTA per tile (grid = tiles_x x tiles_y x batch).  A persistent variant with one-tile-ahead L2
-// bulk prefetch (prefetch_tile) measured slower: the loop raised register pressure.
+// bulk prefetch measured slower: the loop raised register pressure.
 template <int R, int SHAPE, bool LEQ>
 __global__ void __launch_bounds__(32 * ST_BY, ST_MINB) k_rhs(const float* __restrict__ phi, const float* __restrict__ w,
                                                     const float* __restrict__ bv, const float* __restrict__ g,

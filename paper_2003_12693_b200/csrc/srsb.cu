@@ -1,6 +1,15 @@
-// srsb.cu -- context, launch configuration, CUDA graph and C ABI of libsrsb.so.
+// srsb.cu -- contexts, launch configuration, slab exchanges, CUDA graph and C ABI of libsrsb.so.
 // See include/srsb.h for the contract and DESIGN.md for the design.
+//
+// A context holds B images of M_local x N pixels.  Every field is stored with gh ghost rows above
+// and below each image plane; kernels address local row 0 and may read rows -gh .. M_local+gh-1.
+// A whole-image context never reads its ghost rows (periodic neighbours wrap in-kernel).  In slab
+// mode (one image split into P row slabs) the ghost rows are filled by halo
+// exchanges and the FFT's column pass runs on the all-to-all-transposed spectrum; the exchanges
+// are device copies between the slab contexts of one process (LOCAL backend: the single-GPU
+// emulation used by the tests) or NCCL send/recv + all-to-all between processes (one per GPU).
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <cmath>
 #include <cstdio>
@@ -19,6 +28,7 @@ namespace {
 
 constexpr int kMaxWindow = 8;
 constexpr int kGraphIters = 2;   // iterations per captured graph (even: restores the w ping-pong parity)
+enum Backend { BK_NONE = 0, BK_LOCAL = 1, BK_NCCL = 2 };
 
 int ilog2(int v) {
     int r = 0;
@@ -30,14 +40,27 @@ bool is_pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
 }  // namespace
 
 struct sr_sb_ctx {
-    sr_sb_params p;
+    sr_sb_params p;                // p.M = GLOBAL rows
     int device = 0;
     cudaStream_t user = nullptr;   // caller's stream
-    cudaStream_t s = nullptr;      // private work stream (capturable)
+    cudaStream_t s = nullptr;      // work stream (private; shared by the members of a LOCAL group)
+    bool own_stream = true;
     cudaEvent_t ev_in = nullptr, ev_out = nullptr;
-    size_t plane = 0;              // M * N
+    // slab geometry
+    int nranks = 1, rank = 0;      // row slabs of the image, this context's slab
+    int Ml = 0, row_off = 0;       // local rows, global index of local row 0
+    int gh = 1;                    // ghost rows above / below each image plane
+    bool slab = false;             // neighbours of rows 0 / Ml-1 come from ghost rows
+    int backend = BK_NONE;
+    long long pitch = 0;           // floats per image plane (Ml + 2 gh) * N
+    std::vector<sr_sb_ctx*> members;   // LOCAL group leader: the slab contexts (leader has no fields)
+    ncclComm_t comm = nullptr;
+    // fields: *_base = allocation, field = base + gh * N (local row 0 of image 0)
+    float *phi_base = nullptr, *F_base = nullptr, *w_base[2] = {nullptr, nullptr}, *b_base = nullptr,
+          *g_base = nullptr;
     float *phi = nullptr, *F = nullptr, *w[2] = {nullptr, nullptr}, *b = nullptr, *g = nullptr;
-    float2* spec = nullptr;
+    float2* spec = nullptr;        // [B][H/G][Ml][G]
+    float2* spec_cols = nullptr;   // slab: [P][H/(P G)][Ml][G] (all-to-all receive buffer)
     float2 *twH = nullptr, *twM = nullptr, *twR = nullptr;
     float *cM = nullptr, *cN = nullptr;
     int* flag = nullptr;
@@ -81,6 +104,19 @@ thread_local std::string g_create_err;
             return fail(c, SR_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
+#define NK(call)                                                                               \
+    do {                                                                                       \
+        ncclResult_t r_ = (call);                                                              \
+        if (r_ != ncclSuccess)                                                                 \
+            return fail(c, SR_ERR_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_));   \
+    } while (0)
+
+#define RET(x)                          \
+    do {                                \
+        sr_status r_ = (x);             \
+        if (r_ != SR_OK) return r_;     \
+    } while (0)
+
 sr_status validate(const sr_sb_params* p, std::string& msg) {
     if (!p) { msg = "params is NULL"; return SR_ERR_ARG; }
     if (!is_pow2(p->M) || !is_pow2(p->N) || p->M < 8 || p->N < 8 || p->M > 8192 || p->N > 8192) {
@@ -105,9 +141,16 @@ sr_status validate(const sr_sb_params* p, std::string& msg) {
     return SR_OK;
 }
 
+int ghost_rows(const sr_sb_params& p) {
+    const int rblur = (int)std::ceil(3.0 * p.sigma);
+    int gh = p.window > 1 ? p.window : 1;       // window halo, Laplacian / gradient / divergence
+    if (rblur + 1 > gh) gh = rblur + 1;          // edge indicator: blur radius + central difference
+    return gh;
+}
+
 sr_status configure(sr_sb_ctx* c) {
     const sr_sb_params& p = c->p;
-    const int M = p.M, N = p.N, H = N / 2, B = p.batch;
+    const int M = p.M, Ml = c->Ml, N = p.N, H = N / 2, B = p.batch, P = c->nranks;
     const int lgH = ilog2(H), lgM = ilog2(M);
     c->rfwd = pick_row_fwd(lgH);
     c->rinv = pick_row_inv(lgH);
@@ -119,27 +162,28 @@ sr_status configure(sr_sb_ctx* c) {
     int rpc = 8;
     while (rpc * T_h < 64 && rpc < 32) rpc <<= 1;
     while ((rpc * T_h > 512 || rpc * (H + H / 16 + 32) * 8 > 72 * 1024) && rpc > 1) rpc >>= 1;
-    if (rpc > M) rpc = M;
+    if (rpc > Ml) rpc = Ml;
     if (const char* ev = std::getenv("SRSB_RPC")) {   // tuning knob (power of two)
         const int v = std::atoi(ev);
-        if (v >= 1 && v <= M && v * T_h <= 512 && (v & (v - 1)) == 0) rpc = v;
+        if (v >= 1 && v <= Ml && v * T_h <= 512 && (v & (v - 1)) == 0) rpc = v;
     }
     //  column-group interleave of the transposed spectrum: rpc * G >= 8 complex = 64 B contiguous
     int G = 8 / rpc;
     if (G < 1) G = 1;
-    if (G > H) G = H;
+    if (G > H / P) G = H / P;
     if (const char* ev = std::getenv("SRSB_G")) {     // tuning knob (power of two)
         const int v = std::atoi(ev);
-        if (v >= 1 && v <= H && (v & (v - 1)) == 0) G = v;
+        if (v >= 1 && v <= H / P && (v & (v - 1)) == 0) G = v;
     }
     //  columns per CTA: a multiple of G, >= 64 threads, <= 512
+    const int Hl = H / P;                            // spectrum columns this context solves
     const int E_m = M < 16 ? M : 16, T_m = M / E_m;
     int cpc = G;
-    while (cpc * T_m < 64 && cpc * 2 <= H) cpc *= 2;
+    while (cpc * T_m < 64 && cpc * 2 <= Hl) cpc *= 2;
     while (cpc * T_m > 512 && cpc > G) cpc >>= 1;
     if (const char* ev = std::getenv("SRSB_CPC")) {   // tuning knob (power of two, multiple of G)
         const int v = std::atoi(ev);
-        if (v >= G && v <= H && v * T_m <= 512 && (v & (v - 1)) == 0) cpc = v;
+        if (v >= G && v <= Hl && v * T_m <= 512 && (v & (v - 1)) == 0) cpc = v;
     }
     if (cpc * T_m > 512) return fail(c, SR_ERR_SHAPE, "column FFT too large for one CTA");
     auto padded = [](int n, int extra) {   // float2 slots: one pad per 16, rounded to 16, + extra
@@ -147,13 +191,14 @@ sr_status configure(sr_sb_ctx* c) {
         sz = (sz + 15) & ~15;
         return sz + extra;
     };
-    c->ra.M = M;
+    c->ra.plane = c->pitch;
+    c->ra.M = Ml;
     c->ra.lg_rpc = ilog2(rpc);
     c->ra.lg_G = ilog2(G);
     c->ra.SR = padded(H, G < 16 ? G : 1);
     c->ra.clip = 0.f;
     c->ra.accum = 0;
-    c->rgrid = dim3(M / rpc, B, 1);
+    c->rgrid = dim3(Ml / rpc, B, 1);
     c->rblock = dim3(rpc * T_h, 1, 1);
     c->rsmem = rpc * c->ra.SR * (int)sizeof(float2);
     c->ca.H = H;
@@ -162,7 +207,18 @@ sr_status configure(sr_sb_ctx* c) {
     c->ca.SC = padded(M, 1);
     c->ca.taumu = p.tau * p.mu;
     c->ca.scale = (float)(1.0 / ((double)M * (double)H));
-    c->cgrid = dim3(H / cpc, B, 1);
+    if (c->slab) {   // columns of the all-to-all receive buffer: P segments of Ml rows
+        c->ca.lg_seg = ilog2(Ml);
+        c->ca.seg_stride = (long long)Hl * Ml;
+        c->ca.bstride = (long long)H * Ml;           // unused (slab mode has one image)
+        c->ca.k2_off = c->rank * Hl;
+    } else {
+        c->ca.lg_seg = ilog2(M);
+        c->ca.seg_stride = 0;
+        c->ca.bstride = (long long)H * M;
+        c->ca.k2_off = 0;
+    }
+    c->cgrid = dim3(Hl / cpc, B, 1);
     c->cblock = dim3(cpc * T_m, 1, 1);
     c->csmem = cpc * c->ca.SC * (int)sizeof(float2);
     // stencils
@@ -171,12 +227,16 @@ sr_status configure(sr_sb_ctx* c) {
     if (!ok) return fail(c, SR_ERR_ARG, "window radius not supported");
     c->ssmem = smem;
     c->sblock = dim3(32, ST_BY, 1);
-    c->sa.tiles_x = (N + ST_TW - 1) / ST_TW;
-    c->sa.tiles_y = (M + ST_TH - 1) / ST_TH;
-    c->sa.ntiles = c->sa.tiles_x * c->sa.tiles_y * B;
     StencilArgs& a = c->sa;
-    a.M = M;
+    a.tiles_x = (N + ST_TW - 1) / ST_TW;
+    a.tiles_y = (Ml + ST_TH - 1) / ST_TH;
+    a.ntiles = a.tiles_x * a.tiles_y * B;
+    a.M = Ml;
     a.N = N;
+    a.Mg = M;
+    a.row_off = c->row_off;
+    a.slab = c->slab ? 1 : 0;
+    a.plane = c->pitch;
     a.reg.eps = p.epsilon;
     a.reg.inv_eps = 1.f / p.epsilon;
     a.reg.l = p.l;
@@ -201,7 +261,7 @@ sr_status configure(sr_sb_ctx* c) {
     for (int m = 0; m < 2; m++)
         for (int u = 0; u < 2; u++)
             CK(cudaFuncSetAttribute((const void*)c->wb[m][u], cudaFuncAttributeMaxDynamicSharedMemorySize, c->ssmem));
-    c->sgrid = dim3(c->sa.tiles_x, c->sa.tiles_y, B);
+    c->sgrid = dim3(a.tiles_x, a.tiles_y, B);
     return SR_OK;
 }
 
@@ -244,56 +304,176 @@ void prof_end(sr_sb_ctx* c, int cls) {
     c->ev_used += 2;
 }
 
-// phi_out = A^{-1} F (accum = 0) or phi_out += A^{-1} F (accum = 1, increment form), then clamp
-sr_status enq_solve(sr_sb_ctx* c, const float* F, float* out, float clip, int accum) {
+void enq_r2c(sr_sb_ctx* c, const float* F) {
+    prof_begin(c);
+    c->rfwd<<<c->rgrid, c->rblock, c->rsmem, c->s>>>(F, c->spec, c->twH, c->twR, c->ra);
+    prof_end(c, SR_K_ROWS_R2C);
+}
+void enq_cols(sr_sb_ctx* c) {
+    prof_begin(c);
+    c->cols<<<c->cgrid, c->cblock, c->csmem, c->s>>>(c->slab ? c->spec_cols : c->spec, c->twM, c->cM, c->cN, c->ca);
+    prof_end(c, SR_K_COLS_SOLVE);
+}
+void enq_c2r(sr_sb_ctx* c, float* out, float clip, int accum) {
     FftRowArgs ra = c->ra;
     ra.accum = accum;
-    prof_begin(c);
-    c->rfwd<<<c->rgrid, c->rblock, c->rsmem, c->s>>>(F, c->spec, c->twH, c->twR, ra);
-    prof_end(c, SR_K_ROWS_R2C);
-    prof_begin(c);
-    c->cols<<<c->cgrid, c->cblock, c->csmem, c->s>>>(c->spec, c->twM, c->cM, c->cN, c->ca);
-    prof_end(c, SR_K_COLS_SOLVE);
     ra.clip = clip;
     prof_begin(c);
     c->rinv<<<c->rgrid, c->rblock, c->rsmem, c->s>>>(c->spec, out, c->twH, c->twR, ra);
     prof_end(c, SR_K_ROWS_C2R);
-    return SR_OK;
 }
-
-sr_status enq_rhs(sr_sb_ctx* c, float* F) {
+void enq_rhs(sr_sb_ctx* c, float* F) {
     prof_begin(c);
     c->rhs<<<c->sgrid, c->sblock, c->ssmem, c->s>>>(c->phi, c->w[c->wcur], c->b, c->g, F, c->sa);
     prof_end(c, SR_K_RHS);
-    return SR_OK;
+}
+void enq_wb_pass(sr_sb_ctx* c, int last) {
+    prof_begin(c);
+    c->wb[c->p.w_mode][last]<<<c->sgrid, c->sblock, c->ssmem, c->s>>>(c->phi, c->w[c->wcur], c->w[c->wcur ^ 1], c->b,
+                                                                       c->g, c->flag, c->sa);
+    prof_end(c, SR_K_WB);
+    c->wcur ^= 1;
 }
 
-sr_status enq_wb(sr_sb_ctx* c) {
-    const int mode = c->p.w_mode;
-    const int passes = mode == SR_W_FIXED_POINT ? c->p.w_iters : 1;
-    for (int r = 0; r < passes; r++) {
-        const int last = (r == passes - 1) ? 1 : 0;
-        prof_begin(c);
-        c->wb[mode][last]<<<c->sgrid, c->sblock, c->ssmem, c->s>>>(c->phi, c->w[c->wcur], c->w[c->wcur ^ 1], c->b,
-                                                                   c->g, c->flag, c->sa);
-        prof_end(c, SR_K_WB);
-        c->wcur ^= 1;
+// ------------------------------------------------------------------ slab exchanges
+enum HaloField { HF_PHI = 0, HF_W = 1, HF_B = 2, HF_IMG = 3 };
+
+// plane pointer (local row 0) of channel ch of field f (B = 1 in slab mode)
+float* field_rows(sr_sb_ctx* c, int f, int ch) {
+    switch (f) {
+        case HF_PHI: return c->phi;
+        case HF_W: return c->w[c->wcur] + ch * c->pitch;
+        case HF_B: return c->b + ch * c->pitch;
+        default: return c->F;   // HF_IMG: the image staged in F during set_image
+    }
+}
+
+// Ghost-row exchange of field f between the slabs `m` (all slabs for LOCAL, this one for NCCL):
+// A: last gh rows of slab r -> top ghost of r+1;  B: first gh rows of r -> bottom ghost of r-1;
+// C (wrap = phi: the periodic Laplacian rows of Eq. (32)): last rows of P-1 -> top ghost of 0,
+// first rows of 0 -> bottom ghost of P-1.  Same phase order on every rank (NCCL pair matching).
+sr_status halo(std::vector<sr_sb_ctx*>& m, int f, bool wrap) {
+    sr_sb_ctx* c = m[0];
+    const int P = c->nranks, gh = c->gh, N = c->p.N, Ml = c->Ml;
+    const int nch = (f == HF_W || f == HF_B) ? 2 : 1;
+    const size_t cnt = (size_t)gh * N;
+    if (c->backend == BK_LOCAL) {
+        for (int ch = 0; ch < nch; ch++)
+            for (int r = 0; r < P; r++) {
+                sr_sb_ctx* x = m[r];
+                float* rows = field_rows(x, f, ch);
+                if (r + 1 < P) CK(cudaMemcpyAsync(field_rows(m[r + 1], f, ch) - cnt, rows + (size_t)(Ml - gh) * N,
+                                                  cnt * 4, cudaMemcpyDeviceToDevice, x->s));
+                if (r > 0) CK(cudaMemcpyAsync(field_rows(m[r - 1], f, ch) + (size_t)Ml * N, rows, cnt * 4,
+                                              cudaMemcpyDeviceToDevice, x->s));
+                if (wrap && r == P - 1)
+                    CK(cudaMemcpyAsync(field_rows(m[0], f, ch) - cnt, rows + (size_t)(Ml - gh) * N, cnt * 4,
+                                       cudaMemcpyDeviceToDevice, x->s));
+                if (wrap && r == 0)
+                    CK(cudaMemcpyAsync(field_rows(m[P - 1], f, ch) + (size_t)Ml * N, rows, cnt * 4,
+                                       cudaMemcpyDeviceToDevice, x->s));
+            }
+        return SR_OK;
+    }
+    if (c->backend == BK_NCCL) {
+        const int r = c->rank;
+        if (P == 1) {   // a one-rank communicator: only the wrap rows, as local copies
+            if (wrap)
+                for (int ch = 0; ch < nch; ch++) {
+                    float* rows = field_rows(c, f, ch);
+                    CK(cudaMemcpyAsync(rows - cnt, rows + (size_t)(Ml - gh) * N, cnt * 4, cudaMemcpyDeviceToDevice, c->s));
+                    CK(cudaMemcpyAsync(rows + (size_t)Ml * N, rows, cnt * 4, cudaMemcpyDeviceToDevice, c->s));
+                }
+            return SR_OK;
+        }
+        NK(ncclGroupStart());
+        for (int ch = 0; ch < nch; ch++) {
+            float* rows = field_rows(c, f, ch);
+            // A
+            if (r + 1 < P) NK(ncclSend(rows + (size_t)(Ml - gh) * N, cnt, ncclFloat, r + 1, c->comm, c->s));
+            if (r > 0) NK(ncclRecv(rows - cnt, cnt, ncclFloat, r - 1, c->comm, c->s));
+            // B
+            if (r > 0) NK(ncclSend(rows, cnt, ncclFloat, r - 1, c->comm, c->s));
+            if (r + 1 < P) NK(ncclRecv(rows + (size_t)Ml * N, cnt, ncclFloat, r + 1, c->comm, c->s));
+            // C
+            if (wrap) {
+                if (r == P - 1) NK(ncclSend(rows + (size_t)(Ml - gh) * N, cnt, ncclFloat, 0, c->comm, c->s));
+                if (r == 0) NK(ncclRecv(rows - cnt, cnt, ncclFloat, P - 1, c->comm, c->s));
+                if (r == 0) NK(ncclSend(rows, cnt, ncclFloat, P - 1, c->comm, c->s));
+                if (r == P - 1) NK(ncclRecv(rows + (size_t)Ml * N, cnt, ncclFloat, 0, c->comm, c->s));
+            }
+        }
+        NK(ncclGroupEnd());
     }
     return SR_OK;
 }
 
-sr_status enq_iteration(sr_sb_ctx* c) {
+// Spectrum transpose between the row pass and the column pass (fwd) and back (bwd): slab r's
+// block of columns [d H/P, (d+1) H/P) (contiguous in [H/G][Ml][G]) goes to slab d, which stores
+// the P row blocks of its columns as P segments.
+sr_status alltoall(std::vector<sr_sb_ctx*>& m, bool fwd) {
+    sr_sb_ctx* c = m[0];
+    const int P = c->nranks;
+    const size_t blk = (size_t)(c->p.N / 2 / P) * c->Ml;   // complex per (src, dst) pair
+    if (c->backend == BK_LOCAL) {
+        for (int src = 0; src < P; src++)
+            for (int dst = 0; dst < P; dst++) {
+                if (fwd)
+                    CK(cudaMemcpyAsync(m[dst]->spec_cols + src * blk, m[src]->spec + dst * blk, blk * sizeof(float2),
+                                       cudaMemcpyDeviceToDevice, m[src]->s));
+                else
+                    CK(cudaMemcpyAsync(m[src]->spec + dst * blk, m[dst]->spec_cols + src * blk, blk * sizeof(float2),
+                                       cudaMemcpyDeviceToDevice, m[src]->s));
+            }
+        return SR_OK;
+    }
+    if (c->backend == BK_NCCL) {
+        if (fwd) NK(ncclAlltoAll(c->spec, c->spec_cols, 2 * blk, ncclFloat, c->comm, c->s));
+        else NK(ncclAlltoAll(c->spec_cols, c->spec, 2 * blk, ncclFloat, c->comm, c->s));
+    }
+    return SR_OK;
+}
+
+// ------------------------------------------------------------------ the iteration
+sr_status enq_iteration(sr_sb_ctx* c) {   // whole-image context
     for (int s = 0; s < c->p.S; s++) {
         enq_rhs(c, c->F);
-        enq_solve(c, c->F, c->phi, (s == c->p.S - 1) ? c->p.phi_clip : 0.f, 1);
+        enq_r2c(c, c->F);
+        enq_cols(c);
+        enq_c2r(c, c->phi, (s == c->p.S - 1) ? c->p.phi_clip : 0.f, 1);
     }
-    enq_wb(c);
+    const int passes = c->p.w_mode == SR_W_FIXED_POINT ? c->p.w_iters : 1;
+    for (int r = 0; r < passes; r++) enq_wb_pass(c, r == passes - 1);
     return SR_OK;
 }
 
-sr_status check_launch(sr_sb_ctx* c) {
-    CK(cudaGetLastError());
+// slab schedule over the member contexts
+sr_status slab_iteration(std::vector<sr_sb_ctx*>& m) {
+    sr_sb_ctx* c0 = m[0];
+    const sr_sb_params& p = c0->p;
+    for (int s = 0; s < p.S; s++) {
+        RET(halo(m, HF_PHI, true));
+        for (auto* x : m) enq_rhs(x, x->F);
+        for (auto* x : m) enq_r2c(x, x->F);
+        RET(alltoall(m, true));
+        for (auto* x : m) enq_cols(x);
+        RET(alltoall(m, false));
+        for (auto* x : m) enq_c2r(x, x->phi, (s == p.S - 1) ? p.phi_clip : 0.f, 1);
+    }
+    RET(halo(m, HF_PHI, true));
+    const int passes = p.w_mode == SR_W_FIXED_POINT ? p.w_iters : 1;
+    for (int r = 0; r < passes; r++) {
+        if (r > 0) RET(halo(m, HF_W, false));
+        for (auto* x : m) enq_wb_pass(x, r == passes - 1);
+    }
+    RET(halo(m, HF_W, false));
+    RET(halo(m, HF_B, false));
     return SR_OK;
+}
+
+std::vector<sr_sb_ctx*> group_of(sr_sb_ctx* c) {
+    if (c->backend == BK_LOCAL) return c->members;
+    return std::vector<sr_sb_ctx*>{c};
 }
 
 struct DevGuard {
@@ -309,7 +489,7 @@ struct DevGuard {
     }
 };
 
-// order the private stream after the caller's stream, and back
+// order the work stream after the caller's stream, and back
 sr_status begin(sr_sb_ctx* c) {
     CK(cudaEventRecord(c->ev_in, c->user));
     CK(cudaStreamWaitEvent(c->s, c->ev_in, 0));
@@ -322,18 +502,146 @@ sr_status end(sr_sb_ctx* c) {
     return SR_OK;
 }
 
-sr_status copy_in(sr_sb_ctx* c, void* dst, const void* src, size_t bytes) {
-    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->s));
+// copy `nplanes` image planes of Ml rows between a dense caller buffer ([nplanes][Ml][N], host or
+// device) and a field with ghost rows (planes `pitch` floats apart)
+sr_status copy_planes(sr_sb_ctx* c, float* field, const float* dense, int nplanes, bool to_field) {
+    const size_t rowbytes = (size_t)c->Ml * c->p.N * 4;
+    if (to_field)
+        CK(cudaMemcpy2DAsync(field, (size_t)c->pitch * 4, dense, rowbytes, rowbytes, nplanes, cudaMemcpyDefault, c->s));
+    else
+        CK(cudaMemcpy2DAsync(const_cast<float*>(dense), rowbytes, field, (size_t)c->pitch * 4, rowbytes, nplanes,
+                             cudaMemcpyDefault, c->s));
+    return SR_OK;
+}
+
+// ------------------------------------------------------------------ creation
+sr_status create_one(const sr_sb_params* p, int device, cudaStream_t stream, int nranks, int rank, int backend,
+                     cudaStream_t shared_work, sr_sb_ctx** out) {
+    *out = nullptr;
+    sr_sb_ctx* c = new sr_sb_ctx();
+    c->p = *p;
+    c->device = device;
+    c->user = stream;
+    c->nranks = nranks;
+    c->rank = rank;
+    c->backend = backend;
+    c->slab = backend != BK_NONE;
+    c->Ml = p->M / nranks;
+    c->row_off = rank * c->Ml;
+    c->gh = ghost_rows(*p);
+    c->pitch = (long long)(c->Ml + 2 * c->gh) * p->N;
+    const size_t nplane = (size_t)c->pitch * p->batch;           // floats per scalar field
+    const size_t nspec = (size_t)(p->N / 2) * c->Ml * p->batch;  // complex per spectrum
+    auto alloc = [&](void** ptr, size_t bytes) -> bool {
+        if (cudaMalloc(ptr, bytes) != cudaSuccess) { cudaGetLastError(); return false; }
+        return true;
+    };
+    bool ok = true;
+    if (shared_work) {
+        c->s = shared_work;
+        c->own_stream = false;
+    } else {
+        ok = cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking) == cudaSuccess;
+    }
+    ok = ok && cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) { g_create_err = "stream/event creation failed"; sr_sb_destroy(c); return SR_ERR_CUDA; }
+    ok = alloc((void**)&c->phi_base, nplane * 4) && alloc((void**)&c->F_base, nplane * 4) &&
+         alloc((void**)&c->w_base[0], 2 * nplane * 4) && alloc((void**)&c->w_base[1], 2 * nplane * 4) &&
+         alloc((void**)&c->b_base, 2 * nplane * 4) && alloc((void**)&c->g_base, nplane * 4) &&
+         alloc((void**)&c->spec, nspec * sizeof(float2)) && alloc((void**)&c->twH, p->N / 2 * sizeof(float2)) &&
+         alloc((void**)&c->twM, p->M * sizeof(float2)) && alloc((void**)&c->twR, p->N / 2 * sizeof(float2)) &&
+         alloc((void**)&c->cM, p->M * sizeof(float)) && alloc((void**)&c->cN, (p->N / 2 + 1) * sizeof(float)) &&
+         alloc((void**)&c->flag, sizeof(int));
+    if (ok && c->slab) ok = alloc((void**)&c->spec_cols, nspec * sizeof(float2));
+    if (!ok) { g_create_err = "device allocation failed"; sr_sb_destroy(c); return SR_ERR_OOM; }
+    const size_t off = (size_t)c->gh * p->N;
+    c->phi = c->phi_base + off;
+    c->F = c->F_base + off;
+    c->w[0] = c->w_base[0] + off;
+    c->w[1] = c->w_base[1] + off;
+    c->b = c->b_base + off;
+    c->g = c->g_base + off;
+    // ghost rows start defined (zero): never read as data outside the image
+    bool zok = cudaMemsetAsync(c->phi_base, 0, nplane * 4, c->s) == cudaSuccess &&
+               cudaMemsetAsync(c->F_base, 0, nplane * 4, c->s) == cudaSuccess &&
+               cudaMemsetAsync(c->w_base[0], 0, 2 * nplane * 4, c->s) == cudaSuccess &&
+               cudaMemsetAsync(c->w_base[1], 0, 2 * nplane * 4, c->s) == cudaSuccess &&
+               cudaMemsetAsync(c->b_base, 0, 2 * nplane * 4, c->s) == cudaSuccess &&
+               cudaMemsetAsync(c->g_base, 0, nplane * 4, c->s) == cudaSuccess &&
+               cudaMemsetAsync(c->flag, 0, sizeof(int), c->s) == cudaSuccess;
+    if (!zok) { g_create_err = "memset failed"; sr_sb_destroy(c); return SR_ERR_CUDA; }
+    sr_status st = configure(c);
+    if (st == SR_OK) st = make_tables(c);
+    if (st != SR_OK) { g_create_err = c->err; sr_sb_destroy(c); return st; }
+    *out = c;
+    return SR_OK;
+}
+
+sr_status check_device(int device) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        g_create_err = "no CUDA device " + std::to_string(device);
+        return SR_ERR_CUDA;
+    }
+    return SR_OK;
+}
+
+sr_status validate_slab(const sr_sb_params* p, int nranks, std::string& msg) {
+    if (nranks < 1 || !is_pow2(nranks)) { msg = "nranks must be a power of two"; return SR_ERR_ARG; }
+    if (p->batch != 1) { msg = "slab mode decomposes one image: batch must be 1"; return SR_ERR_ARG; }
+    const int Ml = p->M / nranks, gh = ghost_rows(*p);
+    if (Ml < 8 || Ml < gh) { msg = "too many slabs: local rows must be >= 8 and >= the ghost rows"; return SR_ERR_SHAPE; }
+    if ((p->N / 2) % nranks != 0) { msg = "N/2 must be divisible by nranks"; return SR_ERR_SHAPE; }
+    return SR_OK;
+}
+
+// set_image for a list of slab contexts or one whole-image context; image/phi0 already staged
+// into F / phi of each context (local rows)
+sr_status enq_setup(std::vector<sr_sb_ctx*>& m) {
+    sr_sb_ctx* c = m[0];
+    const sr_sb_params& p = c->p;
+    EdgeArgs ea{};
+    ea.N = p.N;
+    ea.Mg = p.M;
+    ea.r = (int)std::ceil(3.0 * p.sigma);
+    double ks = 0.0, kk[17];
+    for (int t = -ea.r; t <= ea.r; t++) { kk[t + ea.r] = std::exp(-(double)t * t / (2.0 * p.sigma * p.sigma)); ks += kk[t + ea.r]; }
+    for (int t = 0; t <= 2 * ea.r; t++) ea.k[t] = (float)(kk[t] / ks);
+    ea.rho = p.rho;
+    ea.s = p.s;
+    ea.plane = c->pitch;
+    if (c->slab) {
+        RET(halo(m, HF_IMG, false));   // image rows for the blur (ghost rows >= r + 1)
+        RET(halo(m, HF_PHI, true));    // phi0 rows for w0 = grad phi0
+    }
+    for (auto* x : m) {
+        EdgeArgs e = ea;
+        e.M = x->Ml;
+        e.row_off = x->row_off;
+        const int ext = x->slab ? ea.r + 1 : 0;
+        float* tmp = x->w[1];   // scratch: free until the first w/b update
+        const dim3 blk(128);
+        e.ext = ext;
+        k_blur_rows<<<dim3((p.N + 127) / 128, x->Ml + 2 * ext, p.batch), blk, 0, x->s>>>(x->F, tmp, e);
+        e.ext = x->slab ? 1 : 0;
+        k_blur_cols<<<dim3((p.N + 127) / 128, x->Ml + 2 * e.ext, p.batch), blk, 0, x->s>>>(tmp, x->F, e);
+        e.ext = 0;
+        k_edge_g<<<dim3((p.N + 127) / 128, x->Ml, p.batch), blk, 0, x->s>>>(x->F, x->g, e);
+        x->wcur = 0;
+        k_init_w<<<dim3((p.N + 127) / 128, x->Ml, p.batch), blk, 0, x->s>>>(x->phi, x->w[0], x->b, p.N, p.M, x->row_off,
+                                                                             x->pitch);
+        sr_sb_ctx* c = x;
+        CK(cudaMemsetAsync(x->flag, 0, sizeof(int), x->s));
+    }
+    if (c->slab) {
+        RET(halo(m, HF_W, false));
+        RET(halo(m, HF_B, false));
+    }
     return SR_OK;
 }
 
 }  // namespace
-
-#define RET(x)                          \
-    do {                                \
-        sr_status r_ = (x);             \
-        if (r_ != SR_OK) return r_;     \
-    } while (0)
 
 extern "C" {
 
@@ -383,70 +691,102 @@ sr_status sr_sb_create(const sr_sb_params* p, int device, void* stream, sr_sb_ct
     std::string msg;
     sr_status st = validate(p, msg);
     if (st != SR_OK) { g_create_err = msg; return st; }
-    int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
-        g_create_err = "no CUDA device " + std::to_string(device);
+    RET(check_device(device));
+    DevGuard dg(device);
+    return create_one(p, device, (cudaStream_t)stream, 1, 0, BK_NONE, nullptr, out);
+}
+
+sr_status sr_sb_create_slab_group(const sr_sb_params* p, int device, void* stream, int nslabs, sr_sb_ctx** out) {
+    if (!out) { g_create_err = "out is NULL"; return SR_ERR_ARG; }
+    *out = nullptr;
+    std::string msg;
+    sr_status st = validate(p, msg);
+    if (st == SR_OK) st = validate_slab(p, nslabs, msg);
+    if (st != SR_OK) { g_create_err = msg; return st; }
+    RET(check_device(device));
+    DevGuard dg(device);
+    sr_sb_ctx* L = new sr_sb_ctx();
+    L->p = *p;
+    L->device = device;
+    L->user = (cudaStream_t)stream;
+    L->nranks = nslabs;
+    L->backend = BK_LOCAL;
+    L->slab = true;
+    L->Ml = p->M;
+    if (cudaStreamCreateWithFlags(&L->s, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&L->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&L->ev_out, cudaEventDisableTiming) != cudaSuccess) {
+        g_create_err = "stream/event creation failed";
+        sr_sb_destroy(L);
         return SR_ERR_CUDA;
     }
-    DevGuard dg(device);
-    sr_sb_ctx* c = new sr_sb_ctx();
-    c->p = *p;
-    c->device = device;
-    c->user = (cudaStream_t)stream;
-    c->plane = (size_t)p->M * p->N;
-    const size_t n = c->plane * p->batch;
-    auto alloc = [&](void** ptr, size_t bytes) -> bool {
-        if (cudaMalloc(ptr, bytes) != cudaSuccess) { cudaGetLastError(); return false; }
-        return true;
-    };
-    bool ok = cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking) == cudaSuccess &&
-              cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming) == cudaSuccess &&
-              cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming) == cudaSuccess;
-    if (!ok) { g_create_err = "stream/event creation failed"; sr_sb_destroy(c); return SR_ERR_CUDA; }
-    ok = alloc((void**)&c->phi, n * 4) && alloc((void**)&c->F, n * 4) && alloc((void**)&c->w[0], 2 * n * 4) &&
-         alloc((void**)&c->w[1], 2 * n * 4) && alloc((void**)&c->b, 2 * n * 4) && alloc((void**)&c->g, n * 4) &&
-         alloc((void**)&c->spec, n / 2 * sizeof(float2)) && alloc((void**)&c->twH, p->N / 2 * sizeof(float2)) &&
-         alloc((void**)&c->twM, p->M * sizeof(float2)) && alloc((void**)&c->twR, p->N / 2 * sizeof(float2)) &&
-         alloc((void**)&c->cM, p->M * sizeof(float)) && alloc((void**)&c->cN, (p->N / 2 + 1) * sizeof(float)) &&
-         alloc((void**)&c->flag, sizeof(int));
-    if (!ok) { g_create_err = "device allocation failed"; sr_sb_destroy(c); return SR_ERR_OOM; }
-    if (cudaMemsetAsync(c->flag, 0, sizeof(int), c->s) != cudaSuccess) {
-        g_create_err = "memset failed"; sr_sb_destroy(c); return SR_ERR_CUDA;
+    for (int r = 0; r < nslabs; r++) {
+        sr_sb_ctx* m = nullptr;
+        st = create_one(p, device, L->s, nslabs, r, BK_LOCAL, L->s, &m);
+        if (st != SR_OK) { sr_sb_destroy(L); return st; }
+        L->members.push_back(m);
     }
-    st = configure(c);
-    if (st == SR_OK) st = make_tables(c);
-    if (st != SR_OK) { g_create_err = c->err; sr_sb_destroy(c); return st; }
-    *out = c;
+    *out = L;
     return SR_OK;
 }
+
+sr_status sr_sb_nccl_unique_id(void* id_out, int bytes) {
+    if (!id_out || bytes < (int)sizeof(ncclUniqueId)) { g_create_err = "need NCCL_UNIQUE_ID_BYTES"; return SR_ERR_ARG; }
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) { g_create_err = ncclGetErrorString(r); return SR_ERR_NCCL; }
+    std::memcpy(id_out, &id, sizeof(id));
+    return SR_OK;
+}
+
+sr_status sr_sb_create_slab_nccl(const sr_sb_params* p, int device, void* stream, int nranks, int rank,
+                                 const void* nccl_id, sr_sb_ctx** out) {
+    if (!out || !nccl_id) { g_create_err = "out and nccl_id must be non-NULL"; return SR_ERR_ARG; }
+    *out = nullptr;
+    std::string msg;
+    sr_status st = validate(p, msg);
+    if (st == SR_OK) st = validate_slab(p, nranks, msg);
+    if (st == SR_OK && (rank < 0 || rank >= nranks)) { msg = "bad rank"; st = SR_ERR_ARG; }
+    if (st != SR_OK) { g_create_err = msg; return st; }
+    RET(check_device(device));
+    DevGuard dg(device);
+    st = create_one(p, device, (cudaStream_t)stream, nranks, rank, BK_NCCL, nullptr, out);
+    if (st != SR_OK) return st;
+    sr_sb_ctx* c = *out;
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+        g_create_err = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+        c->comm = nullptr;
+        sr_sb_destroy(c);
+        *out = nullptr;
+        return SR_ERR_NCCL;
+    }
+    return SR_OK;
+}
+
+int sr_sb_local_rows(const sr_sb_ctx* c) { return c ? c->Ml : -1; }
 
 sr_status sr_sb_set_image(sr_sb_ctx* c, const float* image, const float* phi0) {
     if (!c) return SR_ERR_ARG;
     if (!image || !phi0) return fail(c, SR_ERR_ARG, "image and phi0 must be non-NULL");
     DevGuard dg(c->device);
-    const size_t n = c->plane * c->p.batch;
     RET(begin(c));
-    // F and spec serve as scratch for the one-time edge indicator
-    RET(copy_in(c, c->F, image, n * 4));
-    RET(copy_in(c, c->phi, phi0, n * 4));
-    EdgeArgs ea{};
-    ea.M = c->p.M;
-    ea.N = c->p.N;
-    ea.r = (int)std::ceil(3.0 * c->p.sigma);
-    double ks = 0.0, kk[17];
-    for (int t = -ea.r; t <= ea.r; t++) { kk[t + ea.r] = std::exp(-(double)t * t / (2.0 * c->p.sigma * c->p.sigma)); ks += kk[t + ea.r]; }
-    for (int t = 0; t <= 2 * ea.r; t++) ea.k[t] = (float)(kk[t] / ks);
-    ea.rho = c->p.rho;
-    ea.s = c->p.s;
-    const dim3 blk(128), grd((c->p.N + 127) / 128, c->p.M, c->p.batch);
-    float* tmp = reinterpret_cast<float*>(c->spec);   // n/2 complex = n floats
-    k_blur_rows<<<grd, blk, 0, c->s>>>(c->F, tmp, ea);
-    k_blur_cols<<<grd, blk, 0, c->s>>>(tmp, c->F, ea);
-    k_edge_g<<<grd, blk, 0, c->s>>>(c->F, c->g, ea);
-    c->wcur = 0;
-    k_init_w<<<grd, blk, 0, c->s>>>(c->phi, c->w[0], c->b, c->p.M, c->p.N);
-    CK(cudaMemsetAsync(c->flag, 0, sizeof(int), c->s));
+    std::vector<sr_sb_ctx*> m = group_of(c);
+    for (auto* x : m) {   // LOCAL group: scatter the slabs' rows of the full image
+        const size_t off = (c->backend == BK_LOCAL) ? (size_t)x->row_off * c->p.N : 0;
+        sr_status st = copy_planes(x, x->F, image + off, c->p.batch, true);
+        if (st == SR_OK) st = copy_planes(x, x->phi, phi0 + off, c->p.batch, true);
+        if (st != SR_OK) return fail(c, st, x->err);
+    }
+    sr_status st = enq_setup(m);
+    if (st != SR_OK) return fail(c, st, m[0]->err);
     RET(end(c));
+    for (auto* x : m) {
+        x->k = 0;
+        x->have_state = true;
+    }
     c->k = 0;
     c->have_state = true;
     return SR_OK;
@@ -475,14 +815,24 @@ sr_status sr_sb_iterate(sr_sb_ctx* c, int K) {
     if (K == 0) return SR_OK;
     DevGuard dg(c->device);
     RET(begin(c));
-    int done = 0;
-    if (K >= kGraphIters) {
-        if (!c->graph || c->graph_wcur != c->wcur) RET(build_graph(c));
-        for (; done + kGraphIters <= K; done += kGraphIters) CK(cudaGraphLaunch(c->graph, c->s));
-        // the graph's w ping-pong flips are even, so wcur is unchanged
+    if (c->slab) {   // slab schedule: direct launches + exchanges (no graph)
+        std::vector<sr_sb_ctx*> m = group_of(c);
+        for (int i = 0; i < K; i++) {
+            sr_status st = slab_iteration(m);
+            if (st != SR_OK) return fail(c, st, m[0]->err);
+        }
+    } else {
+        int done = 0;
+        if (K >= kGraphIters) {
+            if (!c->graph || c->graph_wcur != c->wcur) RET(build_graph(c));
+            for (; done + kGraphIters <= K; done += kGraphIters) CK(cudaGraphLaunch(c->graph, c->s));
+            // the graph's w ping-pong flips are even, so wcur is unchanged
+        }
+        for (; done < K; done++) enq_iteration(c);
     }
-    for (; done < K; done++) enq_iteration(c);
     RET(end(c));
+    if (c->backend == BK_LOCAL)
+        for (auto* x : c->members) x->k += K;
     c->k += K;
     return SR_OK;
 }
@@ -492,9 +842,16 @@ sr_status sr_sb_sync(sr_sb_ctx* c) {
     DevGuard dg(c->device);
     CK(cudaStreamSynchronize(c->s));
     CK(cudaStreamSynchronize(c->user));
-    int flag = 0;
-    CK(cudaMemcpy(&flag, c->flag, sizeof(int), cudaMemcpyDeviceToHost));
-    if (flag) return fail(c, SR_ERR_NONFINITE, "non-finite value or |b| > b_max detected in the w/b update");
+    if (c->comm) {
+        ncclResult_t ae = ncclSuccess;
+        NK(ncclCommGetAsyncError(c->comm, &ae));
+        if (ae != ncclSuccess) return fail(c, SR_ERR_NCCL, std::string("NCCL async: ") + ncclGetErrorString(ae));
+    }
+    for (auto* x : group_of(c)) {
+        int flag = 0;
+        CK(cudaMemcpy(&flag, x->flag, sizeof(int), cudaMemcpyDeviceToHost));
+        if (flag) return fail(c, SR_ERR_NONFINITE, "non-finite value or |b| > b_max detected in the w/b update");
+    }
     return SR_OK;
 }
 
@@ -504,7 +861,11 @@ sr_status sr_sb_get_phi(sr_sb_ctx* c, float* phi_out) {
     if (!c->have_state) return fail(c, SR_ERR_STATE, "no state");
     DevGuard dg(c->device);
     RET(begin(c));
-    CK(cudaMemcpyAsync(phi_out, c->phi, c->plane * c->p.batch * 4, cudaMemcpyDefault, c->s));
+    for (auto* x : group_of(c)) {
+        const size_t off = (c->backend == BK_LOCAL) ? (size_t)x->row_off * c->p.N : 0;
+        sr_status st = copy_planes(x, x->phi, phi_out + off, c->p.batch, false);
+        if (st != SR_OK) return fail(c, st, x->err);
+    }
     RET(end(c));
     return SR_OK;
 }
@@ -512,13 +873,18 @@ sr_status sr_sb_get_phi(sr_sb_ctx* c, float* phi_out) {
 sr_status sr_sb_get_state(sr_sb_ctx* c, float* phi, float* w, float* b, float* g) {
     if (!c) return SR_ERR_ARG;
     if (!c->have_state) return fail(c, SR_ERR_STATE, "no state");
+    if (c->backend == BK_LOCAL && (w || b)) return fail(c, SR_ERR_ARG, "slab groups expose phi and g only");
     DevGuard dg(c->device);
-    const size_t n = c->plane * c->p.batch;
     RET(begin(c));
-    if (phi) CK(cudaMemcpyAsync(phi, c->phi, n * 4, cudaMemcpyDefault, c->s));
-    if (w) CK(cudaMemcpyAsync(w, c->w[c->wcur], 2 * n * 4, cudaMemcpyDefault, c->s));
-    if (b) CK(cudaMemcpyAsync(b, c->b, 2 * n * 4, cudaMemcpyDefault, c->s));
-    if (g) CK(cudaMemcpyAsync(g, c->g, n * 4, cudaMemcpyDefault, c->s));
+    for (auto* x : group_of(c)) {
+        const size_t off = (c->backend == BK_LOCAL) ? (size_t)x->row_off * c->p.N : 0;
+        sr_status st = SR_OK;
+        if (phi && st == SR_OK) st = copy_planes(x, x->phi, phi + off, c->p.batch, false);
+        if (w && st == SR_OK) st = copy_planes(x, x->w[x->wcur], w, 2 * c->p.batch, false);
+        if (b && st == SR_OK) st = copy_planes(x, x->b, b, 2 * c->p.batch, false);
+        if (g && st == SR_OK) st = copy_planes(x, x->g, g + off, c->p.batch, false);
+        if (st != SR_OK) return fail(c, st, x->err);
+    }
     RET(end(c));
     return SR_OK;
 }
@@ -527,13 +893,13 @@ sr_status sr_sb_set_state(sr_sb_ctx* c, const float* phi, const float* w, const 
     if (!c) return SR_ERR_ARG;
     if (!phi || !w || !b) return fail(c, SR_ERR_ARG, "phi, w and b must be non-NULL");
     if (!g && !c->have_state) return fail(c, SR_ERR_STATE, "g is required before set_image");
+    if (c->slab) return fail(c, SR_ERR_ARG, "set_state is not available in slab mode");
     DevGuard dg(c->device);
-    const size_t n = c->plane * c->p.batch;
     RET(begin(c));
-    RET(copy_in(c, c->phi, phi, n * 4));
-    RET(copy_in(c, c->w[c->wcur], w, 2 * n * 4));
-    RET(copy_in(c, c->b, b, 2 * n * 4));
-    if (g) RET(copy_in(c, c->g, g, n * 4));
+    RET(copy_planes(c, c->phi, phi, c->p.batch, true));
+    RET(copy_planes(c, c->w[c->wcur], w, 2 * c->p.batch, true));
+    RET(copy_planes(c, c->b, b, 2 * c->p.batch, true));
+    if (g) RET(copy_planes(c, c->g, g, c->p.batch, true));
     CK(cudaMemsetAsync(c->flag, 0, sizeof(int), c->s));
     RET(end(c));
     c->k = 0;
@@ -546,16 +912,16 @@ long long sr_sb_iteration(const sr_sb_ctx* c) { return c ? c->k : -1; }
 sr_status sr_sb_debug_solve(sr_sb_ctx* c, const float* F, float* phi_out) {
     if (!c) return SR_ERR_ARG;
     if (!F || !phi_out) return fail(c, SR_ERR_ARG, "NULL pointer");
+    if (c->slab) return fail(c, SR_ERR_ARG, "debug entries are for whole-image contexts");
     DevGuard dg(c->device);
-    const size_t n = c->plane * c->p.batch;
     RET(begin(c));
-    RET(copy_in(c, c->F, F, n * 4));
-    // solve into F's own buffer is not allowed (rows read F while c2r writes); use a temporary
-    float* tmp = nullptr;
-    CK(cudaMallocAsync((void**)&tmp, n * 4, c->s));
-    enq_solve(c, c->F, tmp, 0.f, 0);
-    CK(cudaMemcpyAsync(phi_out, tmp, n * 4, cudaMemcpyDefault, c->s));
-    CK(cudaFreeAsync(tmp, c->s));
+    RET(copy_planes(c, c->F, F, c->p.batch, true));
+    // solve into F's own buffer is not allowed (rows read F while c2r writes); use w[1] as output
+    float* tmp = c->w[c->wcur ^ 1];
+    enq_r2c(c, c->F);
+    enq_cols(c);
+    enq_c2r(c, tmp, 0.f, 0);
+    RET(copy_planes(c, tmp, phi_out, c->p.batch, false));
     RET(end(c));
     return SR_OK;
 }
@@ -564,10 +930,11 @@ sr_status sr_sb_debug_rhs(sr_sb_ctx* c, float* F_out) {
     if (!c) return SR_ERR_ARG;
     if (!F_out) return fail(c, SR_ERR_ARG, "NULL pointer");
     if (!c->have_state) return fail(c, SR_ERR_STATE, "no state");
+    if (c->slab) return fail(c, SR_ERR_ARG, "debug entries are for whole-image contexts");
     DevGuard dg(c->device);
     RET(begin(c));
     enq_rhs(c, c->F);
-    CK(cudaMemcpyAsync(F_out, c->F, c->plane * c->p.batch * 4, cudaMemcpyDefault, c->s));
+    RET(copy_planes(c, c->F, F_out, c->p.batch, false));
     RET(end(c));
     return SR_OK;
 }
@@ -575,9 +942,11 @@ sr_status sr_sb_debug_rhs(sr_sb_ctx* c, float* F_out) {
 sr_status sr_sb_debug_wb(sr_sb_ctx* c) {
     if (!c) return SR_ERR_ARG;
     if (!c->have_state) return fail(c, SR_ERR_STATE, "no state");
+    if (c->slab) return fail(c, SR_ERR_ARG, "debug entries are for whole-image contexts");
     DevGuard dg(c->device);
     RET(begin(c));
-    enq_wb(c);
+    const int passes = c->p.w_mode == SR_W_FIXED_POINT ? c->p.w_iters : 1;
+    for (int r = 0; r < passes; r++) enq_wb_pass(c, r == passes - 1);
     RET(end(c));
     return SR_OK;
 }
@@ -586,6 +955,7 @@ sr_status sr_sb_profile(sr_sb_ctx* c, int K, float* ms_out, int* launches_out) {
     if (!c) return SR_ERR_ARG;
     if (K < 1 || !ms_out || !launches_out) return fail(c, SR_ERR_ARG, "K >= 1 and non-NULL outputs required");
     if (!c->have_state) return fail(c, SR_ERR_STATE, "profile before set_image/set_state");
+    if (c->slab) return fail(c, SR_ERR_ARG, "profile is for whole-image contexts");
     DevGuard dg(c->device);
     RET(begin(c));
     c->prof = true;
@@ -608,21 +978,26 @@ sr_status sr_sb_profile(sr_sb_ctx* c, int K, float* ms_out, int* launches_out) {
 
 int sr_sb_launches_per_iteration(const sr_sb_ctx* c) {
     if (!c) return -1;
-    return 4 * c->p.S + (c->p.w_mode == SR_W_FIXED_POINT ? c->p.w_iters : 1);
+    const int per = 4 * c->p.S + (c->p.w_mode == SR_W_FIXED_POINT ? c->p.w_iters : 1);
+    return c->backend == BK_LOCAL ? per * (int)c->members.size() : per;
 }
 
 void sr_sb_destroy(sr_sb_ctx* c) {
     if (!c) return;
     DevGuard dg(c->device);
     if (c->s) cudaStreamSynchronize(c->s);
+    for (auto* m : c->members) sr_sb_destroy(m);
+    c->members.clear();
+    if (c->comm) ncclCommDestroy(c->comm);
     if (c->graph) cudaGraphExecDestroy(c->graph);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
-    void* ptrs[] = {c->phi, c->F, c->w[0], c->w[1], c->b, c->g, c->spec, c->twH, c->twM, c->twR, c->cM, c->cN, c->flag};
+    void* ptrs[] = {c->phi_base, c->F_base, c->w_base[0], c->w_base[1], c->b_base, c->g_base, c->spec,
+                    c->spec_cols, c->twH, c->twM, c->twR, c->cM, c->cN, c->flag};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (c->ev_in) cudaEventDestroy(c->ev_in);
     if (c->ev_out) cudaEventDestroy(c->ev_out);
-    if (c->s) cudaStreamDestroy(c->s);
+    if (c->s && c->own_stream) cudaStreamDestroy(c->s);
     delete c;
 }
 

@@ -15,15 +15,18 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("SRSB_LIB", os.path.join(_HERE, "libsrsb.so"))
 
-SR_OK, SR_ERR_ARG, SR_ERR_SHAPE, SR_ERR_CUDA, SR_ERR_NONFINITE, SR_ERR_STATE, SR_ERR_OOM = 0, -1, -2, -3, -5, -6, -7
-STATUS_NAMES = {0: "SR_OK", -1: "SR_ERR_ARG", -2: "SR_ERR_SHAPE", -3: "SR_ERR_CUDA", -5: "SR_ERR_NONFINITE",
-                -6: "SR_ERR_STATE", -7: "SR_ERR_OOM"}
+SR_OK, SR_ERR_ARG, SR_ERR_SHAPE, SR_ERR_CUDA, SR_ERR_NCCL, SR_ERR_NONFINITE, SR_ERR_STATE, SR_ERR_OOM = \
+    0, -1, -2, -3, -4, -5, -6, -7
+STATUS_NAMES = {0: "SR_OK", -1: "SR_ERR_ARG", -2: "SR_ERR_SHAPE", -3: "SR_ERR_CUDA", -4: "SR_ERR_NCCL",
+                -5: "SR_ERR_NONFINITE", -6: "SR_ERR_STATE", -7: "SR_ERR_OOM"}
+NCCL_UNIQUE_ID_BYTES = 128
 
 # every symbol include/srsb.h declares (checked by tests/test_abi.py)
 EXPORTS = ["sr_sb_default_params", "sr_sb_create", "sr_sb_set_image", "sr_sb_iterate", "sr_sb_get_phi",
            "sr_sb_get_state", "sr_sb_set_state", "sr_sb_iteration", "sr_sb_sync", "sr_sb_debug_solve",
            "sr_sb_debug_rhs", "sr_sb_debug_wb", "sr_sb_launches_per_iteration", "sr_sb_destroy",
-           "sr_sb_last_error", "sr_sb_abi_version", "sr_sb_profile"]
+           "sr_sb_last_error", "sr_sb_abi_version", "sr_sb_profile", "sr_sb_create_slab_group",
+           "sr_sb_nccl_unique_id", "sr_sb_create_slab_nccl", "sr_sb_local_rows"]
 KERNEL_CLASSES = ["rhs", "rows_r2c", "cols_solve", "rows_c2r", "wb"]
 
 
@@ -72,6 +75,10 @@ def lib():
             "sr_sb_last_error": (C.c_char_p, [p]),
             "sr_sb_abi_version": (i, []),
             "sr_sb_profile": (st, [p, i, C.POINTER(C.c_float), C.POINTER(C.c_int)]),
+            "sr_sb_create_slab_group": (st, [C.POINTER(Params), i, p, i, C.POINTER(p)]),
+            "sr_sb_nccl_unique_id": (st, [p, i]),
+            "sr_sb_create_slab_nccl": (st, [C.POINTER(Params), i, p, i, i, p, C.POINTER(p)]),
+            "sr_sb_local_rows": (i, [p]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -79,6 +86,15 @@ def lib():
             fn.argtypes = args
         _lib = L
     return _lib
+
+
+def nccl_unique_id() -> bytes:
+    """sr_sb_nccl_unique_id: 128 bytes to broadcast to all ranks before Solver(nccl=...)."""
+    buf = C.create_string_buffer(NCCL_UNIQUE_ID_BYTES)
+    st = lib().sr_sb_nccl_unique_id(C.cast(buf, C.c_void_p), NCCL_UNIQUE_ID_BYTES)
+    if st != SR_OK:
+        raise SrsbError(st, lib().sr_sb_last_error(None).decode())
+    return buf.raw
 
 
 def default_params(M, N, batch=1, window=4) -> dict:
@@ -110,7 +126,9 @@ class Solver:
     library defaults (sr_sb_default_params: DESIGN.md §2).
     """
 
-    def __init__(self, M, N, batch=1, window=4, device=None, stream=None, **params):
+    def __init__(self, M, N, batch=1, window=4, device=None, stream=None, slabs=None, nccl=None, **params):
+        """slabs=P: sr_sb_create_slab_group (P row slabs in this process, full-image buffers).
+        nccl=(nranks, rank, id_bytes): sr_sb_create_slab_nccl (this rank's slab, local-row buffers)."""
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("srsb needs a CUDA device (no CPU fallback)")
@@ -127,10 +145,20 @@ class Solver:
         self.params = {name: getattr(p, name) for name, _ in Params._fields_}
         self.M, self.N, self.batch = M, N, batch
         ctx = C.c_void_p()
-        st = lib().sr_sb_create(C.byref(p), self.device.index, C.c_void_p(stream.cuda_stream), C.byref(ctx))
+        sp = C.c_void_p(stream.cuda_stream)
+        if slabs is not None:
+            st = lib().sr_sb_create_slab_group(C.byref(p), self.device.index, sp, int(slabs), C.byref(ctx))
+        elif nccl is not None:
+            nranks, rank, ident = nccl
+            buf = C.create_string_buffer(bytes(ident), NCCL_UNIQUE_ID_BYTES)
+            st = lib().sr_sb_create_slab_nccl(C.byref(p), self.device.index, sp, int(nranks), int(rank),
+                                              C.cast(buf, C.c_void_p), C.byref(ctx))
+        else:
+            st = lib().sr_sb_create(C.byref(p), self.device.index, sp, C.byref(ctx))
         if st != SR_OK:
             raise SrsbError(st, lib().sr_sb_last_error(None).decode())
         self._ctx = ctx
+        self.M_local = int(lib().sr_sb_local_rows(ctx))
 
     # -- plumbing
     def _check(self, st):
@@ -139,7 +167,8 @@ class Solver:
 
     def _field(self, nch=1):
         import torch
-        return torch.empty((self.batch, nch, self.M, self.N) if nch > 1 else (self.batch, self.M, self.N),
+        M = self.M_local
+        return torch.empty((self.batch, nch, M, self.N) if nch > 1 else (self.batch, M, self.N),
                            dtype=torch.float32, device=self.device)
 
     def close(self):
@@ -172,10 +201,10 @@ class Solver:
         return out
 
     # -- extensions
-    def get_state(self):
-        phi, w, b, g = self._field(), self._field(2), self._field(2), self._field()
-        self._check(lib().sr_sb_get_state(self._ctx, _ptr(phi), _ptr(w), _ptr(b), _ptr(g)))
-        return dict(phi=phi, w=w, b=b, g=g)
+    def get_state(self, fields=("phi", "w", "b", "g")):
+        out = {k: self._field(2 if k in ("w", "b") else 1) for k in fields}
+        self._check(lib().sr_sb_get_state(self._ctx, *[_ptr(out.get(k)) for k in ("phi", "w", "b", "g")]))
+        return out
 
     def set_state(self, phi, w, b, g=None):
         self._check(lib().sr_sb_set_state(self._ctx, _ptr(phi), _ptr(w), _ptr(b), _ptr(g)))

@@ -175,15 +175,14 @@ sr_status configure(sr_sb_ctx* c) {
         const int v = std::atoi(ev);
         if (v >= 1 && v <= H / P && (v & (v - 1)) == 0) G = v;
     }
-    //  columns per CTA: a multiple of G, >= 64 threads, <= 512
+    //  columns per CTA: >= 64 threads, <= 512 (a CTA may cover part of a column group)
     const int Hl = H / P;                            // spectrum columns this context solves
     const int E_m = M < 16 ? M : 16, T_m = M / E_m;
-    int cpc = G;
+    int cpc = 1;
     while (cpc * T_m < 64 && cpc * 2 <= Hl) cpc *= 2;
-    while (cpc * T_m > 512 && cpc > G) cpc >>= 1;
-    if (const char* ev = std::getenv("SRSB_CPC")) {   // tuning knob (power of two, multiple of G)
+    if (const char* ev = std::getenv("SRSB_CPC")) {   // tuning knob (power of two)
         const int v = std::atoi(ev);
-        if (v >= G && v <= Hl && v * T_m <= 512 && (v & (v - 1)) == 0) cpc = v;
+        if (v >= 1 && v <= Hl && v * T_m <= 512 && (v & (v - 1)) == 0) cpc = v;
     }
     if (cpc * T_m > 512) return fail(c, SR_ERR_SHAPE, "column FFT too large for one CTA");
     auto padded = [](int n, int extra) {   // float2 slots: one pad per 16, rounded to 16, + extra

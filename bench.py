@@ -185,8 +185,13 @@ def config_json(cfg, ngpu):
                         f"iterations each, window radius {cfg['window']}, S=3",
             "config_index": cfg["index"], "images": cfg["batch"], "M": cfg["M"], "N": cfg["N"],
             "iterations_per_step": cfg["K"], "window": cfg["window"], "S": 3,
-            "parallelism": f"batch-shard x{ngpu} (images split across GPUs, no collective in the loop)",
-            "l2": "inputs larger than L2 (about 44 B/px of state per GPU)"}
+            "parallelism": {"c3": f"batch-shard x{ngpu} (images split across GPUs, no collective in the loop)",
+                            "c5": (f"slab x{ngpu} (row slabs; NCCL halo send/recv + all-to-all spectrum transpose)"
+                                   if ngpu > 1 else "single GPU, whole image")}.get(
+                cfg["name"], f"replicas x{ngpu} (independent copies of the one-image config)" if ngpu > 1
+                else "single GPU"),
+            "l2": "inputs larger than L2 (44 B/px of state per GPU)" if cfg["name"] != "c1" and cfg["name"] != "c2"
+                  else "L2-resident config (state < 126 MB): latency-bound, not an HBM measurement"}
 
 
 def main():
@@ -214,20 +219,38 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     B = cfg["batch"]
     from paper_2003_12693_b200.dist import max_over_ranks as _max_over_ranks, shard
-    s0, s1 = shard(B, world, rank)
-    mine = list(range(s0, s1))
+    # work split: C3 shards images across ranks; C5 splits its one image into row
+    # slabs (NCCL halos + all-to-all transpose); C1/C2/C4 run as independent replicas
     if args.config == "c3":
-        data = make_config("c3", images=mine)
+        mode = "batch-shard"
+    elif args.config == "c5" and world > 1:
+        mode = "slab"
+    else:
+        mode = "replica" if world > 1 else "single"
+    M, N, K = cfg["M"], cfg["N"], cfg["K"]
+    if mode == "batch-shard":
+        s0, s1 = shard(B, world, rank)
+        data = make_config("c3", images=range(s0, s1))
+        nb = s1 - s0
     else:
         data = make_config(args.config)
-        mine = [0]
-    nb = len(mine)
-    M, N, K = cfg["M"], cfg["N"], cfg["K"]
+        nb = 1
     p = data["params"]
     keys = ("gamma", "alpha", "beta", "mu", "epsilon", "l", "d", "window_shape", "tau", "S", "rho", "sigma",
             "s", "phi_clip", "w_proj", "w_mode", "w_iters")
     stream = torch.cuda.Stream(dev)
-    sv = Solver(M, N, nb, window=p["window"], device=local, stream=stream, **{k: p[k] for k in keys})
+    extra = {}
+    if mode == "slab":
+        from paper_2003_12693_b200.srsb import nccl_unique_id
+        ident = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            ident.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+        torch.distributed.broadcast(ident, 0)
+        extra = dict(nccl=(world, rank, bytes(ident.cpu().numpy())))
+        rows = slice(rank * M // world, (rank + 1) * M // world)
+        data["image"] = np.ascontiguousarray(data["image"][:, rows])
+        data["phi0"] = np.ascontiguousarray(data["phi0"][:, rows])
+    sv = Solver(M, N, nb, window=p["window"], device=local, stream=stream, **{k: p[k] for k in keys}, **extra)
     img_d = torch.from_numpy(data["image"]).to(dev)
     phi0_d = torch.from_numpy(data["phi0"]).to(dev)
     out_d = torch.empty_like(phi0_d)
@@ -264,35 +287,41 @@ def main():
     barrier()
     ms = max_over_ranks(e0.elapsed_time(e1))
     ms_step = ms / args.steps
-    px_total = B * M * N
+    px_total = {"batch-shard": B * M * N, "slab": M * N, "replica": world * M * N, "single": M * N}[mode]
     value = px_total * K * args.steps / (ms / 1e3) / 1e6
 
     # ---------------------------------------------------------------- per-kernel roofline (profile pass)
-    sv.set_image(img_d, phi0_d)
-    prof_iters = 2
-    prof = sv.profile(prof_iters)
-    px_rank = nb * M * N
-    dom = max(prof, key=lambda k: prof[k][0])
-    dom_ms, dom_n = prof[dom]
     peak, peak_src = peaks()
-    achieved = BYTES_PER_PX[dom] * px_rank / (dom_ms / dom_n / 1e3) / 1e9
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
-        t = json.load(open(tpath))
-        if t.get("workload") == args.config and dom in t.get("per_launch_bytes", {}):
-            traffic = t["per_launch_bytes"][dom]
-    iter_ms = sum(v[0] for v in prof.values()) / prof_iters
-    kernels = {k: {"ms_per_launch": v[0] / v[1], "launches_per_iter": v[1] // prof_iters,
-                   "share": v[0] / sum(x[0] for x in prof.values()),
-                   "GBs": BYTES_PER_PX[k] * px_rank / (v[0] / v[1] / 1e3) / 1e9} for k, v in prof.items()}
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                "bytes_per_px_per_launch": BYTES_PER_PX[dom],
-                "step_model": {"bytes_per_px_iter": MODEL_BYTES_PER_PX_ITER,
-                               "achieved_GBs": MODEL_BYTES_PER_PX_ITER * px_rank * K / (ms_step / 1e3) / 1e9,
-                               "frac": MODEL_BYTES_PER_PX_ITER * px_rank * K / (ms_step / 1e3) / 1e9 / peak},
-                "kernels": kernels, "profiled_iteration_ms": iter_ms}
+    px_rank = nb * (M // world if mode == "slab" else M) * N
+    step_model = {"bytes_per_px_iter": MODEL_BYTES_PER_PX_ITER,
+                  "achieved_GBs": MODEL_BYTES_PER_PX_ITER * px_rank * K / (ms_step / 1e3) / 1e9}
+    step_model["frac"] = step_model["achieved_GBs"] / peak
+    if mode != "slab":
+        sv.set_image(img_d, phi0_d)
+        prof_iters = 2
+        prof = sv.profile(prof_iters)
+        dom = max(prof, key=lambda k: prof[k][0])
+        dom_ms, dom_n = prof[dom]
+        achieved = BYTES_PER_PX[dom] * px_rank / (dom_ms / dom_n / 1e3) / 1e9
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tpath):
+            t = json.load(open(tpath))
+            if t.get("workload") == args.config and dom in t.get("per_launch_bytes", {}):
+                traffic = t["per_launch_bytes"][dom]
+        iter_ms = sum(v[0] for v in prof.values()) / prof_iters
+        kernels = {k: {"ms_per_launch": v[0] / v[1], "launches_per_iter": v[1] // prof_iters,
+                       "share": v[0] / sum(x[0] for x in prof.values()),
+                       "GBs": BYTES_PER_PX[k] * px_rank / (v[0] / v[1] / 1e3) / 1e9} for k, v in prof.items()}
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                    "bytes_per_px_per_launch": BYTES_PER_PX[dom], "step_model": step_model,
+                    "kernels": kernels, "profiled_iteration_ms": iter_ms}
+    else:   # slab mode: no per-kernel profile entry; the whole-step model per rank
+        roofline = {"bound": "hbm", "kernel": "step (slab: kernels + NCCL halos / all-to-all)",
+                    "achieved": step_model["achieved_GBs"], "peak": peak, "unit": "GB/s",
+                    "frac": step_model["frac"], "traffic": None, "peak_source": peak_src,
+                    "bytes_per_px_per_launch": None, "step_model": step_model}
 
     # ---------------------------------------------------------------- end to end through host buffers
     e2e = None
@@ -329,8 +358,9 @@ def main():
         cpu = cpu_baseline_oracle(cfg)
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-               "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
-               "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config_json(cfg, world),
+               "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+               "scaling": "weak" if mode == "replica" else "strong",
+               "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": dict(config_json(cfg, world), mode=mode),
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches * world,
                "clocks": clk.summary()}
         print(json.dumps(out), flush=True)

@@ -258,21 +258,32 @@ __device__ __forceinline__ void stage_u(float4* __restrict__ U, const float* __r
     using TG = TileGeom<R>;
     const int tid = threadIdx.y * 32 + threadIdx.x;
     constexpr int NTH = 32 * ST_BY;
-    constexpr int TOT = TG::ROWS * TG::CH;
-#pragma unroll 4
-    for (int e = tid; e < TOT; e += NTH) {
-        const int r = e / TG::CH, f = e - r * TG::CH;
-        const int gi = row0 - R + r, gj = col0 - TG::RA + 2 * f;
+    // each thread owns one chunk column f for rows r = tid / CH, + RPP, + 2 RPP, ...: the column
+    // bounds test and the column part of the address are computed once, rows advance by pointer
+    // increments (no per-element division)
+    constexpr int RPP = NTH / TG::CH;                    // rows covered per pass
+    static_assert(RPP >= 1, "tile too wide for the CTA");
+    const int f = tid % TG::CH, r_first = tid / TG::CH;
+    if (r_first >= RPP) return;                          // the NTH % CH leftover threads
+    const int gj = col0 - TG::RA + 2 * f;
+    const bool col_in = gj >= 0 && gj < N;
+    int gi = row0 - R + r_first;
+    long long o = (long long)gi * N + gj;                // gi may address a ghost row
+    float4* dst = U + r_first * TG::LDC + swz(f);
+#pragma unroll 2
+    for (int r = r_first; r < TG::ROWS; r += RPP) {
         float4 A = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (gi + row_off >= 0 && gi + row_off < Mg && gj >= 0 && gj < N) {
-            const long long o = (long long)gi * N + gj;   // gi may address a ghost row
+        if (col_in && gi + row_off >= 0 && gi + row_off < Mg) {
             const float2 P = __ldg(reinterpret_cast<const float2*>(phi + o));
             const float2 X = __ldg(reinterpret_cast<const float2*>(w1 + o));
             const float2 Y = __ldg(reinterpret_cast<const float2*>(w2 + o));
             const float h0 = reg_h<LEQ>(P.x, reg), h1 = reg_h<LEQ>(P.y, reg);
             A = make_float4(h0 * X.x, h0 * Y.x, h1 * X.y, h1 * Y.y);
         }
-        U[r * TG::LDC + swz(f)] = A;
+        *dst = A;
+        gi += RPP;
+        o += (long long)RPP * N;
+        dst += RPP * TG::LDC;
     }
 }
 

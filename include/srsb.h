@@ -155,6 +155,25 @@ typedef enum { SR_K_RHS = 0, SR_K_ROWS_R2C = 1, SR_K_COLS_SOLVE = 2, SR_K_ROWS_C
  * host.  Advances the state exactly like sr_sb_iterate(ctx, K). */
 sr_status sr_sb_profile(sr_sb_ctx* ctx, int K, float* ms_out, int* launches_out);
 
+/* ---- Monitoring and convergence (whole-image contexts).
+ * sr_sb_set_monitor(ctx, 1) makes every outer iteration also accumulate, per image, in double:
+ *   [0] E_g = sum g |w| delta(phi)            [1] E_a = sum g (1 - H(phi))
+ *   [2] E_r = -sum_x sum_{y in W(x)} G w(x).w(y) h(phi(x)) h(phi(y))
+ *   [3] E_pen = (mu/2) sum |w - grad phi - b|^2                     (the terms of Eq. (22) at the
+ *       state (phi^{k+1}, w^k, b^k) entering the w-update; total = gamma[0] + alpha[1] + beta[2] + [3])
+ *   [4 + 2s], [5 + 2s] = ||phi^{k+1,s+1} - phi^{k+1,s}||^2 and ||phi^{k+1,s}||^2 for sweep s
+ * for the LAST iteration enqueued.  sr_sb_get_monitor copies [batch][4 + 2 S] doubles (synchronous).
+ * sr_sb_iterate_until runs up to K_max iterations in chunks of `every`, stopping after the first
+ * chunk with ||phi^k - phi^{k-every}|| / (||phi^{k-every}|| + 1e-6) <= tol for every image (the
+ * relative phi change; Alg. 1's outer test "(13) converges", is unspecified; the inner
+ * sweep rule of P:366 is reported by the monitor but is not a fixed-point test under the clamp:
+ * the sweeps push phi past +-1 and the clamp resets it).  *k_done = iterations run;
+ * sr_sb_last_change returns the last measured relative change. */
+sr_status sr_sb_set_monitor(sr_sb_ctx* ctx, int enable);
+sr_status sr_sb_get_monitor(sr_sb_ctx* ctx, double* out);
+sr_status sr_sb_iterate_until(sr_sb_ctx* ctx, int K_max, double tol, int every, int* k_done);
+double sr_sb_last_change(const sr_sb_ctx* ctx);
+
 /* Number of kernel launches one outer iteration enqueues (for bench accounting). */
 int sr_sb_launches_per_iteration(const sr_sb_ctx* ctx);
 

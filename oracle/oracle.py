@@ -18,7 +18,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 
 __all__ = ["build", "Params", "H", "delta", "delta_prime", "h", "h_prime", "grad", "div", "edge",
            "fft", "fft2", "symbol", "solve", "window_sum", "rhs", "shrink", "project", "wb",
-           "init", "sweep", "iterate", "label", "run", "lib"]
+           "init", "sweep", "iterate", "label", "run", "lib", "energy"]
 
 
 def build(force: bool = False) -> str:
@@ -53,6 +53,7 @@ def lib():
             "orc_sweep": (i, [i, i, p, p, p, p, p, p, p]),
             "orc_iterate": (i, [i, i, p, p, p, p, p, p, p, i]),
             "orc_label": (i, [i, i, p, i, p]),
+            "orc_energy": (None, [i, i, p, p, p, p, p, p, p, p]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(_lib, name)
@@ -230,6 +231,15 @@ def iterate(p, state, g, K):
     if bad:
         raise FloatingPointError(f"{bad} solves failed the imaginary-part check (Q11)")
     return state
+
+
+def energy(p, phi, w1, w2, b1, b2, g):
+    """(E_g, E_a, E_r, E_pen) of Eq. (22) at (phi, w, b); total = gamma E_g + alpha E_a + beta E_r + E_pen."""
+    phi, w1, w2, b1, b2, g = map(_d, (phi, w1, w2, b1, b2, g))
+    M, N = phi.shape
+    out = np.zeros(4)
+    lib().orc_energy(M, N, _P(p), _ptr(phi), _ptr(w1), _ptr(w2), _ptr(b1), _ptr(b2), _ptr(g), _ptr(out))
+    return tuple(out)
 
 
 def label(mask, conn=4):

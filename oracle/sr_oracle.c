@@ -418,6 +418,43 @@ void orc_wb(int M, int N, const orc_params *P, const double *phi,
 }
 
 /* ------------------------------------------------------------------ */
+/* Energy of the split problem, Eq. (22) (NEXT-1 monitoring)           */
+/* ------------------------------------------------------------------ */
+
+/* Terms of E(phi, w) in Eq. (22) at the state (phi, w, b), discretized on the pixel grid:
+ *   out[0] = E_g   = sum_x g |w| delta(phi)                         (first line, / gamma)
+ *   out[1] = E_a   = sum_x g (1 - H(phi))                            (first line, / alpha)
+ *   out[2] = E_r   = - sum_x sum_{y in W(x)} G(x-y) w(x).w(y) h(phi(x)) h(phi(y))   (second line, / beta)
+ *   out[3] = E_pen = (mu/2) sum_x |w - grad phi - b|^2               (third line)
+ * The library reports them at the state entering the w-update: (phi^{k+1}, w^k, b^k). */
+void orc_energy(int M, int N, const orc_params *P, const double *phi, const double *w1, const double *w2,
+                const double *b1, const double *b2, const double *g, double *out)
+{
+    size_t n = (size_t)M * N;
+    double *u1 = malloc(sizeof(double) * n), *u2 = malloc(sizeof(double) * n);
+    double *v1 = malloc(sizeof(double) * n), *v2 = malloc(sizeof(double) * n);
+    double *gp1 = malloc(sizeof(double) * n), *gp2 = malloc(sizeof(double) * n);
+    for (size_t q = 0; q < n; q++) {
+        double hq = orc_h(phi[q], P->epsilon, P->l);
+        u1[q] = hq * w1[q];
+        u2[q] = hq * w2[q];
+    }
+    orc_window_sum(M, N, P->window, P->d, P->window_shape, u1, u2, v1, v2);
+    orc_grad(M, N, phi, gp1, gp2);
+    double eg = 0.0, ea = 0.0, er = 0.0, ep = 0.0;
+    for (size_t q = 0; q < n; q++) {
+        double wn = sqrt(w1[q] * w1[q] + w2[q] * w2[q]);
+        eg += g[q] * wn * orc_delta(phi[q], P->epsilon);
+        ea += g[q] * (1.0 - orc_H(phi[q], P->epsilon));
+        er -= u1[q] * v1[q] + u2[q] * v2[q];     /* h(x) w(x) . sum_y G w(y) h(y) */
+        double r1 = w1[q] - gp1[q] - b1[q], r2 = w2[q] - gp2[q] - b2[q];
+        ep += 0.5 * P->mu * (r1 * r1 + r2 * r2);
+    }
+    out[0] = eg; out[1] = ea; out[2] = er; out[3] = ep;
+    free(u1); free(u2); free(v1); free(v2); free(gp1); free(gp2);
+}
+
+/* ------------------------------------------------------------------ */
 /* Algorithm 1                                              */
 /* ------------------------------------------------------------------ */
 

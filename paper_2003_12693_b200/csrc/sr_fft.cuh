@@ -151,6 +151,8 @@ struct FftRowArgs {
     int SR;         // float2 per shared row, padded
     float clip;     // c2r only: > 0 clamps the output to [-clip, clip]
     int accum;      // c2r only: 1 -> phi = phi + z (increment form), 0 -> phi = z
+    double* stats;  // c2r monitor: per image [.., sum (phi_new - phi_old)^2, sum phi_old^2] at `stats` (null = off)
+    int stats_stride;
 };
 
 // Row pass 1: F rows (N = 2H reals) -> transposed packed half spectrum.
@@ -339,6 +341,7 @@ __global__ void __launch_bounds__(512) k_rows_c2r(const float2* __restrict__ spe
     }
     __syncthreads();
     fft_stages<LOGH, LOGE, 0, true>(v, sm, t, twH);
+    float dsum = 0.f, osum = 0.f;
 #pragma unroll
     for (int u = 0; u < E; u++) {
         float2 z = v[u];
@@ -351,6 +354,28 @@ __global__ void __launch_bounds__(512) k_rows_c2r(const float2* __restrict__ spe
             z.y = fminf(fmaxf(z.y, -a.clip), a.clip);
         }
         out[t + u * T] = z;
+        if (a.stats && a.accum) {   // NEXT-1: ||phi^{s+1} - phi^s||^2 and ||phi^s||^2
+            const float dx = z.x - old[u].x, dy = z.y - old[u].y;
+            dsum += dx * dx + dy * dy;
+            osum += old[u].x * old[u].x + old[u].y * old[u].y;
+        }
+    }
+    if (a.stats && a.accum) {
+        double* st = a.stats + (long long)b * a.stats_stride;
+        if ((blockDim.x & 31) == 0) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+                osum += __shfl_xor_sync(0xffffffffu, osum, o);
+            }
+            if ((tid & 31) == 0) {
+                atomicAdd(st, (double)dsum);
+                atomicAdd(st + 1, (double)osum);
+            }
+        } else {
+            atomicAdd(st, (double)dsum);
+            atomicAdd(st + 1, (double)osum);
+        }
     }
 }
 

@@ -88,4 +88,30 @@ __global__ void k_init_w(const float* __restrict__ phi, float* __restrict__ w, f
     b1[plane + o] = 0.f;
 }
 
+// NEXT-1 outer convergence: per image sum (phi - prev)^2 and sum prev^2 over the local rows, then
+// prev = phi.  grid (blocks, batch); out[img * stride + 0 / 1].
+__global__ void k_phi_change(const float* __restrict__ phi, float* __restrict__ prev, double* __restrict__ out,
+                             int M, int N, long long plane, int stride) {
+    const int img = blockIdx.y;
+    const float* p = phi + img * plane;
+    float* q = prev + img * plane;
+    float d2 = 0.f, o2 = 0.f;
+    const long long n = (long long)M * N;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const float a = p[i], b = q[i];
+        d2 += (a - b) * (a - b);
+        o2 += b * b;
+        q[i] = a;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        d2 += __shfl_xor_sync(0xffffffffu, d2, o);
+        o2 += __shfl_xor_sync(0xffffffffu, o2, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(out + (long long)img * stride, (double)d2);
+        atomicAdd(out + (long long)img * stride + 1, (double)o2);
+    }
+}
+
 }  // namespace srsb

@@ -180,8 +180,21 @@ struct StencilArgs {
     float gamma_mu;    // gamma / mu
     int w_proj;        // 0 ball, 1 sphere, 2 none
     float b_max;
-    int tiles_x, tiles_y, ntiles;   // persistent tile loop: tiles per row, per column, total (x batch)
+    int tiles_x, tiles_y, ntiles;   // tiles per row, per column, total (x batch)
+    double* stats;     // NEXT-1 monitor: per image [E_g, E_a, E_r, E_pen, ...] accumulated by k_wb; null = off
+    int stats_stride;  // doubles per image in stats
 };
+
+// warp-sum of v, one double atomicAdd per warp (monitor only); partial warps add per thread
+__device__ __forceinline__ void warp_accumulate(double* dst, float v) {
+    if (__activemask() == 0xffffffffu) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) == 0) atomicAdd(dst, (double)v);
+    } else {
+        atomicAdd(dst, (double)v);
+    }
+}
 
 #ifndef SRSB_ST_RT
 #define SRSB_ST_RT 8
@@ -476,6 +489,7 @@ __device__ __forceinline__ void wb_tile(float4* __restrict__ U, const float* __r
     window_block<R, SHAPE>(U, r0, c0, a.e, v);
     bool bad = false;
     constexpr int CT = ST_CT;
+    float e_g = 0.f, e_a = 0.f, e_r = 0.f, e_pen = 0.f;   // monitor partial sums (Eq. 22 terms)
 #pragma unroll
     for (int i = 0; i < ST_RT; i++) {
         const int gi = row0 + r0 + i;
@@ -508,6 +522,16 @@ __device__ __forceinline__ void wb_tile(float4* __restrict__ U, const float* __r
             const float gp2 = (j < N - 1) ? p_[c + 1] - ps : 0.f;
             float x, y, hh, dd;
             reg_hd<LEQ>(ps, a.reg, hh, dd);
+            if (a.stats) {   // energy of Eq. (22) at (phi^{k+1}, w^k, b^k), the state entering the update
+                const float wa = __ldg(w1 + o + c), wb2 = __ldg(w2 + o + c);
+                const float aa = ps * a.reg.inv_eps;
+                const float H = aa > 1.f ? 1.f : (aa < -1.f ? 0.f : 0.5f * (1.f + aa + sinpif(aa) * (1.f / kPi)));
+                e_g += g_[c] * sqrtf(wa * wa + wb2 * wb2) * dd;
+                e_a += g_[c] * (1.f - H);
+                e_r -= hh * (wa * v[i][c].x + wb2 * v[i][c].y);
+                const float r1 = wa - gp1 - b1_[c], r2 = wb2 - gp2 - b2_[c];
+                e_pen += 0.5f * a.mu * (r1 * r1 + r2 * r2);
+            }
             if (MODE == 0) {
                 const float Bx = gp1 + b1_[c] + a.beta2_mu * hh * v[i][c].x;
                 const float By = gp2 + b2_[c] + a.beta2_mu * hh * v[i][c].y;
@@ -545,6 +569,13 @@ __device__ __forceinline__ void wb_tile(float4* __restrict__ U, const float* __r
         }
     }
     if (UPDATE_B && bad) atomicOr(flag, 1);
+    if (UPDATE_B && a.stats) {
+        double* st = a.stats + (long long)img * a.stats_stride;
+        warp_accumulate(st + 0, e_g);
+        warp_accumulate(st + 1, e_a);
+        warp_accumulate(st + 2, e_r);
+        warp_accumulate(st + 3, e_pen);
+    }
 }
 
 // One CTA per tile (grid = tiles_x x tiles_y x batch).  A persistent variant with one-tile-ahead L2

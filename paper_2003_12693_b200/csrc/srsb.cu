@@ -81,6 +81,12 @@ struct sr_sb_ctx {
     StencilArgs sa{};
     dim3 rgrid, rblock, cgrid, cblock, sgrid, sblock;
     int rsmem = 0, csmem = 0, ssmem = 0;
+    // NEXT-1 monitor: per image [E_g, E_a, E_r, E_pen, (|dphi_s|^2, |phi_s|^2) x S]
+    double* stats = nullptr;
+    int stats_stride = 0;
+    float* prev_phi = nullptr;     // phi at the previous convergence check (sr_sb_iterate_until)
+    double last_change = -1.0;     // outer relative change measured at the last check
+    double* conv = nullptr;        // [batch][2] sums of the outer change
     // sr_sb_profile
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -313,10 +319,12 @@ void enq_cols(sr_sb_ctx* c) {
     c->cols<<<c->cgrid, c->cblock, c->csmem, c->s>>>(c->slab ? c->spec_cols : c->spec, c->twM, c->cM, c->cN, c->ca);
     prof_end(c, SR_K_COLS_SOLVE);
 }
-void enq_c2r(sr_sb_ctx* c, float* out, float clip, int accum) {
+void enq_c2r(sr_sb_ctx* c, float* out, float clip, int accum, int sweep = -1) {
     FftRowArgs ra = c->ra;
     ra.accum = accum;
     ra.clip = clip;
+    ra.stats = (c->stats && sweep >= 0) ? c->stats + 4 + 2 * sweep : nullptr;
+    ra.stats_stride = c->stats_stride;
     prof_begin(c);
     c->rinv<<<c->rgrid, c->rblock, c->rsmem, c->s>>>(c->spec, out, c->twH, c->twR, ra);
     prof_end(c, SR_K_ROWS_C2R);
@@ -435,11 +443,12 @@ sr_status alltoall(std::vector<sr_sb_ctx*>& m, bool fwd) {
 
 // ------------------------------------------------------------------ the iteration
 sr_status enq_iteration(sr_sb_ctx* c) {   // whole-image context
+    if (c->stats) cudaMemsetAsync(c->stats, 0, sizeof(double) * c->stats_stride * c->p.batch, c->s);
     for (int s = 0; s < c->p.S; s++) {
         enq_rhs(c, c->F);
         enq_r2c(c, c->F);
         enq_cols(c);
-        enq_c2r(c, c->phi, (s == c->p.S - 1) ? c->p.phi_clip : 0.f, 1);
+        enq_c2r(c, c->phi, (s == c->p.S - 1) ? c->p.phi_clip : 0.f, 1, s);
     }
     const int passes = c->p.w_mode == SR_W_FIXED_POINT ? c->p.w_iters : 1;
     for (int r = 0; r < passes; r++) enq_wb_pass(c, r == passes - 1);
@@ -975,6 +984,80 @@ sr_status sr_sb_profile(sr_sb_ctx* c, int K, float* ms_out, int* launches_out) {
     return SR_OK;
 }
 
+sr_status sr_sb_set_monitor(sr_sb_ctx* c, int enable) {
+    if (!c) return SR_ERR_ARG;
+    if (c->slab) return fail(c, SR_ERR_ARG, "the monitor is for whole-image contexts");
+    DevGuard dg(c->device);
+    CK(cudaStreamSynchronize(c->s));
+    if (enable && !c->stats) {
+        c->stats_stride = 4 + 2 * c->p.S;
+        CK(cudaMalloc((void**)&c->stats, sizeof(double) * c->stats_stride * c->p.batch));
+        CK(cudaMemset(c->stats, 0, sizeof(double) * c->stats_stride * c->p.batch));
+        CK(cudaMalloc((void**)&c->prev_phi, sizeof(float) * c->pitch * c->p.batch));
+        CK(cudaMemset(c->prev_phi, 0, sizeof(float) * c->pitch * c->p.batch));
+        CK(cudaMalloc((void**)&c->conv, sizeof(double) * 2 * c->p.batch));
+    } else if (!enable && c->stats) {
+        CK(cudaFree(c->stats));
+        CK(cudaFree(c->prev_phi));
+        CK(cudaFree(c->conv));
+        c->stats = nullptr;
+        c->prev_phi = nullptr;
+        c->conv = nullptr;
+    }
+    c->sa.stats = c->stats;
+    c->sa.stats_stride = c->stats_stride;
+    if (c->graph) {   // the captured graph bakes the kernel arguments: rebuild on the next iterate
+        cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
+    }
+    return SR_OK;
+}
+
+sr_status sr_sb_get_monitor(sr_sb_ctx* c, double* out) {
+    if (!c || !out) return SR_ERR_ARG;
+    if (!c->stats) return fail(c, SR_ERR_STATE, "monitor not enabled (sr_sb_set_monitor)");
+    DevGuard dg(c->device);
+    CK(cudaStreamSynchronize(c->s));
+    CK(cudaMemcpy(out, c->stats, sizeof(double) * c->stats_stride * c->p.batch, cudaMemcpyDeviceToHost));
+    return SR_OK;
+}
+
+sr_status sr_sb_iterate_until(sr_sb_ctx* c, int K_max, double tol, int every, int* k_done) {
+    if (!c) return SR_ERR_ARG;
+    if (K_max < 0 || every < 1 || !(tol >= 0.0)) return fail(c, SR_ERR_ARG, "need K_max >= 0, every >= 1, tol >= 0");
+    if (!c->stats) return fail(c, SR_ERR_STATE, "monitor not enabled (sr_sb_set_monitor)");
+    DevGuard dg(c->device);
+    const int B = c->p.batch;
+    const dim3 grd(64, B), blk(256);
+    const size_t off = (size_t)c->gh * c->p.N;
+    std::vector<double> cv(2 * B);
+    // snapshot phi^k
+    CK(cudaMemsetAsync(c->conv, 0, sizeof(double) * 2 * B, c->s));
+    k_phi_change<<<grd, blk, 0, c->s>>>(c->phi, c->prev_phi + off, c->conv, c->Ml, c->p.N, c->pitch, 2);
+    int done = 0;
+    while (done < K_max) {
+        const int n = (K_max - done) < every ? (K_max - done) : every;
+        RET(sr_sb_iterate(c, n));
+        done += n;
+        // outer relative change ||phi^k - phi^{k-n}|| / (||phi^{k-n}|| + 1e-6)  (SPEC's outer rule)
+        CK(cudaMemsetAsync(c->conv, 0, sizeof(double) * 2 * B, c->s));
+        k_phi_change<<<grd, blk, 0, c->s>>>(c->phi, c->prev_phi + off, c->conv, c->Ml, c->p.N, c->pitch, 2);
+        CK(cudaMemcpyAsync(cv.data(), c->conv, sizeof(double) * 2 * B, cudaMemcpyDeviceToHost, c->s));
+        CK(cudaStreamSynchronize(c->s));
+        double worst = 0.0;
+        for (int b = 0; b < B; b++) {
+            const double r = std::sqrt(cv[2 * b]) / (std::sqrt(cv[2 * b + 1]) + 1e-6);
+            if (r > worst) worst = r;
+        }
+        c->last_change = worst;
+        if (worst <= tol) break;
+    }
+    if (k_done) *k_done = done;
+    return SR_OK;
+}
+
+double sr_sb_last_change(const sr_sb_ctx* c) { return c ? c->last_change : -1.0; }
+
 int sr_sb_launches_per_iteration(const sr_sb_ctx* c) {
     if (!c) return -1;
     const int per = 4 * c->p.S + (c->p.w_mode == SR_W_FIXED_POINT ? c->p.w_iters : 1);
@@ -991,7 +1074,7 @@ void sr_sb_destroy(sr_sb_ctx* c) {
     if (c->graph) cudaGraphExecDestroy(c->graph);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     void* ptrs[] = {c->phi_base, c->F_base, c->w_base[0], c->w_base[1], c->b_base, c->g_base, c->spec,
-                    c->spec_cols, c->twH, c->twM, c->twR, c->cM, c->cN, c->flag};
+                    c->spec_cols, c->twH, c->twM, c->twR, c->cM, c->cN, c->flag, c->stats, c->prev_phi, c->conv};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (c->ev_in) cudaEventDestroy(c->ev_in);

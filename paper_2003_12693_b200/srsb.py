@@ -26,7 +26,8 @@ EXPORTS = ["sr_sb_default_params", "sr_sb_create", "sr_sb_set_image", "sr_sb_ite
            "sr_sb_get_state", "sr_sb_set_state", "sr_sb_iteration", "sr_sb_sync", "sr_sb_debug_solve",
            "sr_sb_debug_rhs", "sr_sb_debug_wb", "sr_sb_launches_per_iteration", "sr_sb_destroy",
            "sr_sb_last_error", "sr_sb_abi_version", "sr_sb_profile", "sr_sb_create_slab_group",
-           "sr_sb_nccl_unique_id", "sr_sb_create_slab_nccl", "sr_sb_local_rows"]
+           "sr_sb_nccl_unique_id", "sr_sb_create_slab_nccl", "sr_sb_local_rows", "sr_sb_set_monitor",
+           "sr_sb_get_monitor", "sr_sb_iterate_until", "sr_sb_last_change"]
 KERNEL_CLASSES = ["rhs", "rows_r2c", "cols_solve", "rows_c2r", "wb"]
 
 
@@ -79,6 +80,10 @@ def lib():
             "sr_sb_nccl_unique_id": (st, [p, i]),
             "sr_sb_create_slab_nccl": (st, [C.POINTER(Params), i, p, i, i, p, C.POINTER(p)]),
             "sr_sb_local_rows": (i, [p]),
+            "sr_sb_set_monitor": (st, [p, i]),
+            "sr_sb_get_monitor": (st, [p, C.POINTER(C.c_double)]),
+            "sr_sb_iterate_until": (st, [p, i, C.c_double, i, C.POINTER(C.c_int)]),
+            "sr_sb_last_change": (C.c_double, [p]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -226,6 +231,30 @@ class Solver:
         n = (C.c_int * 5)()
         self._check(lib().sr_sb_profile(self._ctx, int(K), ms, n))
         return {name: (float(ms[i]), int(n[i])) for i, name in enumerate(KERNEL_CLASSES)}
+
+    def set_monitor(self, enable=True):
+        self._check(lib().sr_sb_set_monitor(self._ctx, int(bool(enable))))
+
+    def monitor(self):
+        """Per image: dict(E_g, E_a, E_r, E_pen, E_total, sweep_change=[..S]) of the last iteration."""
+        S = self.params["S"]
+        buf = (C.c_double * ((4 + 2 * S) * self.batch))()
+        self._check(lib().sr_sb_get_monitor(self._ctx, buf))
+        out = []
+        p = self.params
+        for k in range(self.batch):
+            x = buf[k * (4 + 2 * S):(k + 1) * (4 + 2 * S)]
+            ch = [(x[4 + 2 * s] ** 0.5) / ((x[5 + 2 * s] ** 0.5) + 1e-6) for s in range(S)]
+            out.append(dict(E_g=x[0], E_a=x[1], E_r=x[2], E_pen=x[3],
+                            E_total=p["gamma"] * x[0] + p["alpha"] * x[1] + p["beta"] * x[2] + x[3],
+                            sweep_change=ch, raw=list(x)))
+        return out
+
+    def iterate_until(self, K_max, tol, every=10):
+        """sr_sb_iterate_until: returns (iterations run, last relative phi change)."""
+        k = C.c_int(0)
+        self._check(lib().sr_sb_iterate_until(self._ctx, int(K_max), float(tol), int(every), C.byref(k)))
+        return k.value, float(lib().sr_sb_last_change(self._ctx))
 
     def debug_solve(self, F):
         out = self._field()

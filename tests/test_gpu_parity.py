@@ -268,3 +268,59 @@ def test_nonfinite_guard(S):
         with pytest.raises(S.SrsbError) as ei:
             sv.sync()
         assert ei.value.status == S.SR_ERR_NONFINITE
+
+
+# ----------------------------------------------------------------------------- NEXT-1 monitor
+def test_monitor_energy_and_sweep_changes(S, orc):
+    """Energies of Eq. (22) at (phi^{k+1}, w^k, b^k) and the per-sweep phi changes of one
+    teacher-forced iteration, against the oracle."""
+    from synth import random_state
+    M, N = 128, 256
+    st = random_state(M, N, batch=2, seed=21)
+    p = _params(4)
+    with _solver(S, M, N, 2, p) as sv:
+        w = np.stack([st["w1"], st["w2"]], 1)
+        b = np.stack([st["b1"], st["b2"]], 1)
+        sv.set_state(_cuda(st["phi"]), _cuda(w), _cuda(b), _cuda(st["g"]))
+        sv.set_monitor(True)
+        sv.iterate(1)
+        mon = sv.monitor()
+    for k in range(2):
+        psi = st["phi"][k].astype(np.float64)
+        args = [st[n][k] for n in ("w1", "w2", "b1", "b2", "g")]
+        changes = []
+        for s in range(p["S"]):
+            new = orc.sweep(p, psi, *args)
+            if s == p["S"] - 1:
+                new = np.clip(new, -p["phi_clip"], p["phi_clip"])
+            changes.append(np.linalg.norm(new - psi) / (np.linalg.norm(psi) + 1e-6))
+            psi = new
+        eg, ea, er, ep = orc.energy(p, psi, *args)
+        got = mon[k]
+        for a, r in ((got["E_g"], eg), (got["E_a"], ea), (got["E_r"], er), (got["E_pen"], ep)):
+            assert a == pytest.approx(r, rel=1e-4, abs=1e-3)
+        assert got["sweep_change"] == pytest.approx(changes, rel=1e-3)
+
+
+def test_iterate_until_outer_change(S, orc):
+    """sr_sb_iterate_until stops at the first check whose relative phi change (over `every`
+    iterations) is <= tol; the reported change matches the oracle trajectory's at that point."""
+    from synth import make_config
+    cfg = make_config("c1")
+    p = cfg["params"]
+    with _solver(S, 128, 128, 1, p) as sv:
+        sv.set_image(_cuda(cfg["image"]), _cuda(cfg["phi0"]))
+        sv.set_monitor(True)
+        k, ch = sv.iterate_until(60, 0.0, every=20)          # tol 0: runs all 60, reports the change
+        assert k == 60 and sv.iteration == 60 and ch > 0
+        phi = _np(sv.get_phi())[0]
+        k2, ch2 = sv.iterate_until(200, 10.0, every=20)      # huge tol: stops after the first chunk
+        assert k2 == 20
+    g = orc.edge(cfg["image"][0], p["sigma"], p["rho"], p["s"])
+    st = orc.init(cfg["phi0"][0])
+    orc.iterate(p, st, g, 40)
+    a = st["phi"].copy()
+    orc.iterate(p, st, g, 20)
+    ref = np.linalg.norm(st["phi"] - a) / (np.linalg.norm(a) + 1e-6)
+    assert ch == pytest.approx(ref, rel=5e-3, abs=1e-5)
+    assert np.max(np.abs(phi - st["phi"])) < 1e-2

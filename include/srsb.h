@@ -162,7 +162,8 @@ sr_status sr_sb_profile(sr_sb_ctx* ctx, int K, float* ms_out, int* launches_out)
  *   [3] E_pen = (mu/2) sum |w - grad phi - b|^2                     (the terms of Eq. (22) at the
  *       state (phi^{k+1}, w^k, b^k) entering the w-update; total = gamma[0] + alpha[1] + beta[2] + [3])
  *   [4 + 2s], [5 + 2s] = ||phi^{k+1,s+1} - phi^{k+1,s}||^2 and ||phi^{k+1,s}||^2 for sweep s
- * for the LAST iteration enqueued.  sr_sb_get_monitor copies [batch][4 + 2 S] doubles (synchronous).
+ * for the LAST iteration enqueued (energies in the threshold w-mode).  sr_sb_get_monitor copies
+ * [batch][4 + 2 S] doubles (synchronous).
  * sr_sb_iterate_until runs up to K_max iterations in chunks of `every`, stopping after the first
  * chunk with ||phi^k - phi^{k-every}|| / (||phi^{k-every}|| + 1e-6) <= tol for every image (the
  * relative phi change; Alg. 1's outer test "(13) converges", is unspecified; the inner

@@ -16,9 +16,9 @@ RowKernel pick_row_fwd(int log2_h);       // fft_r2c.cu
 RowInvKernel pick_row_inv(int log2_h);    // fft_c2r.cu
 ColKernel pick_col(int log2_m);           // fft_cols.cu
 // stencil_r<R>.cu; returns false if R is unsupported.  smem = dynamic shared bytes.
-bool pick_stencil(int R, int shape, bool leq, RhsKernel& rhs, WbKernel (&wb)[2][2], int& smem);
+bool pick_stencil(int R, int shape, bool leq, RhsKernel& rhs, WbKernel (&wb)[2][2], WbKernel& wb_mon, int& smem);
 
-#define SRSB_DECLARE_STENCIL(R) bool pick_stencil_r##R(int shape, bool leq, RhsKernel& rhs, WbKernel (&wb)[2][2], int& smem);
+#define SRSB_DECLARE_STENCIL(R) bool pick_stencil_r##R(int shape, bool leq, RhsKernel& rhs, WbKernel (&wb)[2][2], WbKernel& wb_mon, int& smem);
 SRSB_DECLARE_STENCIL(0) SRSB_DECLARE_STENCIL(1) SRSB_DECLARE_STENCIL(2) SRSB_DECLARE_STENCIL(3)
 SRSB_DECLARE_STENCIL(4) SRSB_DECLARE_STENCIL(5) SRSB_DECLARE_STENCIL(6) SRSB_DECLARE_STENCIL(7)
 SRSB_DECLARE_STENCIL(8)

@@ -205,7 +205,10 @@ __device__ __forceinline__ void warp_accumulate(double* dst, float v) {
 constexpr int ST_CT = 2;            // columns per thread
 constexpr int ST_RT = SRSB_ST_RT;   // rows per thread
 constexpr int ST_BY = SRSB_ST_BY;   // thread rows per CTA
-constexpr int ST_MINB = 32 / ST_BY; // resident CTAs per SM the register budget targets (<= 64 regs)
+#ifndef SRSB_ST_MINB
+#define SRSB_ST_MINB (32 / SRSB_ST_BY)
+#endif
+constexpr int ST_MINB = SRSB_ST_MINB;  // resident CTAs per SM the register budget targets (4: <= 64 regs)
 constexpr int ST_TW = 32 * ST_CT;
 constexpr int ST_TH = ST_BY * ST_RT;
 
@@ -464,7 +467,7 @@ __device__ __forceinline__ void project_w(int mode, float& x, float& y) {
 // MODE 0: threshold (Eq. 41-42); MODE 1: fixed-point sweep (Eq. 38-39).  UPDATE_B: last pass,
 // b += grad phi - w_new (Eq. 23) and the non-finite guard.  w_in is read for v (the halo) only in
 // mode 1 beyond the pixel; in mode 0 w_in = w^k.  b is updated in place (pixel-local).
-template <int R, int SHAPE, int MODE, bool UPDATE_B, bool LEQ>
+template <int R, int SHAPE, int MODE, bool UPDATE_B, bool LEQ, bool MON>
 __device__ __forceinline__ void wb_tile(float4* __restrict__ U, const float* __restrict__ phi,
                                         const float* __restrict__ w_in, float* __restrict__ w_out,
                                         float* __restrict__ bv, const float* __restrict__ g,
@@ -522,7 +525,7 @@ __device__ __forceinline__ void wb_tile(float4* __restrict__ U, const float* __r
             const float gp2 = (j < N - 1) ? p_[c + 1] - ps : 0.f;
             float x, y, hh, dd;
             reg_hd<LEQ>(ps, a.reg, hh, dd);
-            if (a.stats) {   // energy of Eq. (22) at (phi^{k+1}, w^k, b^k), the state entering the update
+            if (MON) {   // energy of Eq. (22) at (phi^{k+1}, w^k, b^k), the state entering the update
                 const float wa = __ldg(w1 + o + c), wb2 = __ldg(w2 + o + c);
                 const float aa = ps * a.reg.inv_eps;
                 const float H = aa > 1.f ? 1.f : (aa < -1.f ? 0.f : 0.5f * (1.f + aa + sinpif(aa) * (1.f / kPi)));
@@ -569,7 +572,7 @@ __device__ __forceinline__ void wb_tile(float4* __restrict__ U, const float* __r
         }
     }
     if (UPDATE_B && bad) atomicOr(flag, 1);
-    if (UPDATE_B && a.stats) {
+    if (MON) {
         double* st = a.stats + (long long)img * a.stats_stride;
         warp_accumulate(st + 0, e_g);
         warp_accumulate(st + 1, e_a);
@@ -588,13 +591,15 @@ __global__ void __launch_bounds__(32 * ST_BY, ST_MINB) k_rhs(const float* __rest
     rhs_tile<R, SHAPE, LEQ>(U, phi, w, bv, g, D, a, blockIdx.z, blockIdx.y, blockIdx.x);
 }
 
-template <int R, int SHAPE, int MODE, bool UPDATE_B, bool LEQ>
+// MON: the NEXT-1 monitor variant (Eq. 22 energy partial sums), used only when monitoring is on
+template <int R, int SHAPE, int MODE, bool UPDATE_B, bool LEQ, bool MON = false>
 __global__ void __launch_bounds__(32 * ST_BY, ST_MINB) k_wb(const float* __restrict__ phi, const float* __restrict__ w_in,
                                                    float* __restrict__ w_out, float* __restrict__ bv,
                                                    const float* __restrict__ g, int* __restrict__ flag,
                                                    StencilArgs a) {
     extern __shared__ float4 U[];
-    wb_tile<R, SHAPE, MODE, UPDATE_B, LEQ>(U, phi, w_in, w_out, bv, g, flag, a, blockIdx.z, blockIdx.y, blockIdx.x);
+    wb_tile<R, SHAPE, MODE, UPDATE_B, LEQ, MON>(U, phi, w_in, w_out, bv, g, flag, a, blockIdx.z, blockIdx.y,
+                                                blockIdx.x);
 }
 
 }  // namespace srsb

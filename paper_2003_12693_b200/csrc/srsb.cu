@@ -76,6 +76,7 @@ struct sr_sb_ctx {
     ColKernel cols = nullptr;
     RhsKernel rhs = nullptr;
     WbKernel wb[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+    WbKernel wb_mon = nullptr;     // monitor variant (threshold mode, last pass)
     FftRowArgs ra{};
     FftColArgs ca{};
     StencilArgs sa{};
@@ -228,7 +229,7 @@ sr_status configure(sr_sb_ctx* c) {
     c->csmem = cpc * c->ca.SC * (int)sizeof(float2);
     // stencils
     int smem = 0;
-    bool ok = pick_stencil(p.window, p.window_shape, p.l == p.epsilon, c->rhs, c->wb, smem);
+    bool ok = pick_stencil(p.window, p.window_shape, p.l == p.epsilon, c->rhs, c->wb, c->wb_mon, smem);
     if (!ok) return fail(c, SR_ERR_ARG, "window radius not supported");
     c->ssmem = smem;
     c->sblock = dim3(32, ST_BY, 1);
@@ -266,6 +267,7 @@ sr_status configure(sr_sb_ctx* c) {
     for (int m = 0; m < 2; m++)
         for (int u = 0; u < 2; u++)
             CK(cudaFuncSetAttribute((const void*)c->wb[m][u], cudaFuncAttributeMaxDynamicSharedMemorySize, c->ssmem));
+    CK(cudaFuncSetAttribute((const void*)c->wb_mon, cudaFuncAttributeMaxDynamicSharedMemorySize, c->ssmem));
     c->sgrid = dim3(a.tiles_x, a.tiles_y, B);
     return SR_OK;
 }
@@ -336,8 +338,8 @@ void enq_rhs(sr_sb_ctx* c, float* F) {
 }
 void enq_wb_pass(sr_sb_ctx* c, int last) {
     prof_begin(c);
-    c->wb[c->p.w_mode][last]<<<c->sgrid, c->sblock, c->ssmem, c->s>>>(c->phi, c->w[c->wcur], c->w[c->wcur ^ 1], c->b,
-                                                                       c->g, c->flag, c->sa);
+    WbKernel k = (c->stats && last && c->p.w_mode == SR_W_THRESHOLD) ? c->wb_mon : c->wb[c->p.w_mode][last];
+    k<<<c->sgrid, c->sblock, c->ssmem, c->s>>>(c->phi, c->w[c->wcur], c->w[c->wcur ^ 1], c->b, c->g, c->flag, c->sa);
     prof_end(c, SR_K_WB);
     c->wcur ^= 1;
 }

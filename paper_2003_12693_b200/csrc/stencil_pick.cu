@@ -1,17 +1,17 @@
 // Dispatch on the window radius R (P:368 summation radius, 0..8).
 #include "sr_kernels.h"
 namespace srsb {
-bool pick_stencil(int R, int shape, bool leq, RhsKernel& rhs, WbKernel (&wb)[2][2], int& smem) {
+bool pick_stencil(int R, int shape, bool leq, RhsKernel& rhs, WbKernel (&wb)[2][2], WbKernel& wb_mon, int& smem) {
     switch (R) {
-        case 0: return pick_stencil_r0(shape, leq, rhs, wb, smem);
-        case 1: return pick_stencil_r1(shape, leq, rhs, wb, smem);
-        case 2: return pick_stencil_r2(shape, leq, rhs, wb, smem);
-        case 3: return pick_stencil_r3(shape, leq, rhs, wb, smem);
-        case 4: return pick_stencil_r4(shape, leq, rhs, wb, smem);
-        case 5: return pick_stencil_r5(shape, leq, rhs, wb, smem);
-        case 6: return pick_stencil_r6(shape, leq, rhs, wb, smem);
-        case 7: return pick_stencil_r7(shape, leq, rhs, wb, smem);
-        case 8: return pick_stencil_r8(shape, leq, rhs, wb, smem);
+        case 0: return pick_stencil_r0(shape, leq, rhs, wb, wb_mon, smem);
+        case 1: return pick_stencil_r1(shape, leq, rhs, wb, wb_mon, smem);
+        case 2: return pick_stencil_r2(shape, leq, rhs, wb, wb_mon, smem);
+        case 3: return pick_stencil_r3(shape, leq, rhs, wb, wb_mon, smem);
+        case 4: return pick_stencil_r4(shape, leq, rhs, wb, wb_mon, smem);
+        case 5: return pick_stencil_r5(shape, leq, rhs, wb, wb_mon, smem);
+        case 6: return pick_stencil_r6(shape, leq, rhs, wb, wb_mon, smem);
+        case 7: return pick_stencil_r7(shape, leq, rhs, wb, wb_mon, smem);
+        case 8: return pick_stencil_r8(shape, leq, rhs, wb, wb_mon, smem);
     }
     return false;
 }

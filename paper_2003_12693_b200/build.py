@@ -60,7 +60,22 @@ def _compile(src: str, force: bool) -> tuple[str, str]:
     return obj, "built"
 
 
+LIB_STAMP = LIB + ".flags"
+
+
+def _up_to_date() -> bool:
+    """The .so is newer than every source/header and was linked with the current flags."""
+    if not (os.path.exists(LIB) and os.path.exists(LIB_STAMP)):
+        return False
+    if open(LIB_STAMP).read() != " ".join(ARCH + FLAGS + LDFLAGS):
+        return False
+    newest = max(os.path.getmtime(p) for p in glob.glob(os.path.join(CSRC, "*.cu")) + _deps())
+    return os.path.getmtime(LIB) >= newest
+
+
 def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -> str:
+    if not force and _up_to_date():
+        return LIB
     os.makedirs(OBJ, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     jobs = jobs or max(1, os.cpu_count() or 1)
@@ -74,6 +89,8 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -
         cmd = [NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart"] + LDFLAGS
         subprocess.check_call(cmd)
         os.replace(tmp, LIB)
+        with open(LIB_STAMP, "w") as f:
+            f.write(" ".join(ARCH + FLAGS + LDFLAGS))
     if verbose:
         for s, (_, st) in zip(srcs, results):
             print(f"{os.path.basename(s)}: {st}")

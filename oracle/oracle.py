@@ -18,7 +18,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 
 __all__ = ["build", "Params", "H", "delta", "delta_prime", "h", "h_prime", "grad", "div", "edge",
            "fft", "fft2", "symbol", "solve", "window_sum", "rhs", "shrink", "project", "wb",
-           "init", "sweep", "iterate", "label", "run", "lib", "energy"]
+           "init", "sweep", "iterate", "label", "run", "lib", "energy", "thomas_neumann", "solve_aos"]
 
 
 def build(force: bool = False) -> str:
@@ -54,6 +54,8 @@ def lib():
             "orc_iterate": (i, [i, i, p, p, p, p, p, p, p, i]),
             "orc_label": (i, [i, i, p, i, p]),
             "orc_energy": (None, [i, i, p, p, p, p, p, p, p, p]),
+            "orc_thomas_neumann": (None, [i, d, p, p]),
+            "orc_solve_aos": (None, [i, i, d, d, p, p]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(_lib, name)
@@ -67,13 +69,13 @@ class Params(C.Structure):
     _fields_ = [("gamma", C.c_double), ("alpha", C.c_double), ("beta", C.c_double), ("mu", C.c_double),
                 ("epsilon", C.c_double), ("l", C.c_double), ("d", C.c_double), ("window", C.c_int),
                 ("window_shape", C.c_int), ("tau", C.c_double), ("S", C.c_int), ("phi_clip", C.c_double),
-                ("w_proj", C.c_int), ("w_mode", C.c_int), ("w_iters", C.c_int)]
+                ("w_proj", C.c_int), ("w_mode", C.c_int), ("w_iters", C.c_int), ("phi_solver", C.c_int)]
 
     @classmethod
     def from_dict(cls, p: dict) -> "Params":
         q = cls()
         for name, _ in cls._fields_:
-            setattr(q, name, p[name])
+            setattr(q, name, p.get(name, 0) if name == "phi_solver" else p[name])
         return q
 
 
@@ -163,6 +165,23 @@ def solve(F, tau, mu, check=True):
     bad = lib().orc_solve(M, N, tau, mu, _ptr(F), _ptr(phi))
     if check and bad:
         raise FloatingPointError("imaginary part of the solve exceeds 1e-12 max|F| (Q11)")
+    return phi
+
+
+def thomas_neumann(f, c):
+    """(I - c A) x = f on one line, A the Neumann 1-D second difference (Thomas algorithm)."""
+    f = _d(f)
+    x = np.empty_like(f)
+    lib().orc_thomas_neumann(len(f), c, _ptr(f), _ptr(x))
+    return x
+
+
+def solve_aos(F, tau, mu):
+    """AOS phi solve of P:427: 1/2 [(I - 2 tau mu A_1)^-1 + (I - 2 tau mu A_2)^-1] F."""
+    F = _d(F)
+    M, N = F.shape
+    phi = np.empty_like(F)
+    lib().orc_solve_aos(M, N, tau, mu, _ptr(F), _ptr(phi))
     return phi
 
 

@@ -18,6 +18,7 @@
  *   - edge indicator: Eq. (1) with a normalized Gaussian of radius ceil(3 sigma) (Q16);
  *   - FFT: recursive radix-2 complex DFT, unnormalized forward, 1/n inverse;
  *   - phi solve: Eq. (31)-(33), full complex 2-D FFT, divide by the symbol of Eq. (32) (Q10);
+ *     or the AOS variant of P:427 (Thomas solves of the Neumann 1-D operators, NEXT-4);
  *   - window sum: the direct double loop of P:368 (disc or square window, Q2, Q5);
  *   - RHS: Eq. (37) with phi^{k+1,s} in every term (Q8);
  *   - w/b update: Eq. (41), (42), projection Eq. (40) as BALL/SPHERE/NONE (Q1), Eq. (23);
@@ -53,6 +54,7 @@ typedef struct {
     int w_proj;                      /* 0 BALL, 1 SPHERE, 2 NONE (Q1) */
     int w_mode;                      /* 0 threshold Eq. (41)-(42); 1 fixed point Eq. (38)-(39) */
     int w_iters;                     /* fixed-point sweeps r = 0..w_iters-1 */
+    int phi_solver;                  /* 0 FFT, Eq. (31)-(33); 1 AOS with constant coefficients (NEXT-4) */
 } orc_params;
 
 #define IDX(i, j) ((size_t)(i) * (size_t)N + (size_t)(j))
@@ -274,6 +276,62 @@ int orc_solve(int M, int N, double tau, double mu, const double *F, double *phi)
 }
 
 /* ------------------------------------------------------------------ */
+/* phi sub-problem by AOS (the AOS splitting of Eq. (19)-(20)) */
+/* ------------------------------------------------------------------ */
+
+/* Solve (I - c A) x = f for one line of n values, A the 1-D second difference with Neumann
+ * (reflecting) ends: (A x)_0 = x_1 - x_0, (A x)_{n-1} = x_{n-2} - x_{n-1}.  Thomas algorithm
+ * (LR decomposition, forward and backward substitution). */
+void orc_thomas_neumann(int n, double c, const double *f, double *x)
+{
+    if (n == 1) { x[0] = f[0]; return; }
+    double *cp = malloc(sizeof(double) * n), *y = malloc(sizeof(double) * n);
+    const double a = -c;                       /* sub- and super-diagonal */
+    double d = 1.0 + c;                        /* first row: 1 - c (x_1 - x_0) -> diag 1 + c */
+    cp[0] = a / d;
+    y[0] = f[0] / d;
+    for (int i = 1; i < n; i++) {
+        d = (i == n - 1 ? 1.0 + c : 1.0 + 2.0 * c) - a * cp[i - 1];
+        cp[i] = a / d;
+        y[i] = (f[i] - a * y[i - 1]) / d;
+    }
+    x[n - 1] = y[n - 1];
+    for (int i = n - 2; i >= 0; i--) x[i] = y[i] - cp[i] * x[i + 1];
+    free(cp); free(y);
+}
+
+/* AOS: phi = 1/2 [ (I - 2 tau mu A_1)^{-1} + (I - 2 tau mu A_2)^{-1} ] F, A_1 along columns
+ * (index i), A_2 along rows (index j), m = 2 directions (the splitting of Eq. (19)-(20) with the
+ * constant coefficients of the phi sub-problem). */
+void orc_solve_aos(int M, int N, double tau, double mu, const double *F, double *phi)
+{
+    const double c = 2.0 * tau * mu;
+    double *x1 = malloc(sizeof(double) * (size_t)M * N);
+    #pragma omp parallel
+    {
+        double *col = malloc(sizeof(double) * M), *sol = malloc(sizeof(double) * M);
+        #pragma omp for schedule(static)
+        for (int j = 0; j < N; j++) {
+            for (int i = 0; i < M; i++) col[i] = F[IDX(i, j)];
+            orc_thomas_neumann(M, c, col, sol);
+            for (int i = 0; i < M; i++) x1[IDX(i, j)] = sol[i];
+        }
+        free(col); free(sol);
+    }
+    #pragma omp parallel
+    {
+        double *sol = malloc(sizeof(double) * N);
+        #pragma omp for schedule(static)
+        for (int i = 0; i < M; i++) {
+            orc_thomas_neumann(N, c, F + IDX(i, 0), sol);
+            for (int j = 0; j < N; j++) phi[IDX(i, j)] = 0.5 * (x1[IDX(i, j)] + sol[j]);
+        }
+        free(sol);
+    }
+    free(x1);
+}
+
+/* ------------------------------------------------------------------ */
 /* Non-local window sum, P:368-369 (and Eq. 38)                        */
 /* ------------------------------------------------------------------ */
 
@@ -475,7 +533,9 @@ int orc_sweep(int M, int N, const orc_params *P, double *psi, const double *w1, 
     size_t n = (size_t)M * N;
     double *F = malloc(sizeof(double) * n);
     orc_rhs(M, N, P, psi, w1, w2, b1, b2, g, F);
-    int bad = orc_solve(M, N, P->tau, P->mu, F, psi);
+    int bad = 0;
+    if (P->phi_solver == 1) orc_solve_aos(M, N, P->tau, P->mu, F, psi);
+    else bad = orc_solve(M, N, P->tau, P->mu, F, psi);
     free(F);
     return bad;
 }

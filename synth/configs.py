@@ -50,7 +50,7 @@ def paper_params(window: int, **over) -> dict:
     shape = int(over.get("window_shape", 0))
     p = dict(gamma=1.0, alpha=4.0, beta=repulsion_beta(window, d, shape), mu=8.0, epsilon=0.5, l=0.5,
              d=d, window=int(window), window_shape=shape, tau=0.05, S=3,
-             rho=30.0, sigma=1.0, s=2, phi_clip=1.0, w_proj=0, w_mode=0, w_iters=1)
+             rho=30.0, sigma=1.0, s=2, phi_clip=1.0, w_proj=0, w_mode=0, w_iters=1, phi_solver=0)
     p.update(over)
     return p
 

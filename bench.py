@@ -30,7 +30,8 @@ sys.path.insert(0, ROOT)
 METRIC = "megapixel-iterations/s per SB-SR iteration"
 UNIT = "Mpx-iter/s"
 # algorithmic HBM bytes per pixel per launch of each kernel class
-BYTES_PER_PX = {"rhs": 28.0, "rows_r2c": 8.0, "cols_solve": 8.0, "rows_c2r": 12.0, "wb": 40.0}
+BYTES_PER_PX = {"rhs": 28.0, "rows_r2c": 8.0, "cols_solve": 8.0, "rows_c2r": 12.0, "wb": 40.0,
+                "aos_vert": 8.0, "aos_horiz": 12.0}   # aos_vert: register-chunk kernel (M <= 2048)
 MODEL_BYTES_PER_PX_ITER = 172.0   # SURVEY.md §8(d) fused model (S = 3)
 
 
@@ -43,6 +44,8 @@ def parse():
     ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--images", type=int, default=None, help="override the batch (C3 only)")
     ap.add_argument("--iters", type=int, default=None, help="override iterations per step")
+    ap.add_argument("--phi-solver", default="fft", choices=["fft", "aos"],
+                    help="phi sub-problem: FFT solve Eq. (31)-(33) (north star) or the AOS variant (P:427)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
@@ -63,6 +66,7 @@ def workload(args):
         cfg["batch"] = args.images
     if args.iters:
         cfg["K"] = args.iters
+    cfg["phi_solver"] = {"fft": 0, "aos": 1}[args.phi_solver]
     return cfg
 
 
@@ -127,7 +131,7 @@ def cpu_baseline_oracle(cfg, target_s=12.0):
     cores = len(os.sched_getaffinity(0))
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
     c = make_config(cfg["name"], images=[0]) if cfg["name"] == "c3" else make_config(cfg["name"])
-    p = c["params"]
+    p = dict(c["params"], phi_solver=cfg["phi_solver"])
     img, phi0 = c["image"][0], c["phi0"][0]
     M, N = img.shape
     g = oracle.edge(img, p["sigma"], p["rho"], p["s"])
@@ -157,7 +161,7 @@ def run_reference(args, cfg, rank):
     cores = len(os.sched_getaffinity(0))
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
     c = make_config(cfg["name"], images=[0]) if cfg["name"] == "c3" else make_config(cfg["name"])
-    p = c["params"]
+    p = dict(c["params"], phi_solver=cfg["phi_solver"])
     img, phi0 = c["image"][0], c["phi0"][0]
     M, N = img.shape
     g = oracle.edge(img, p["sigma"], p["rho"], p["s"])
@@ -185,6 +189,7 @@ def config_json(cfg, ngpu):
                         f"iterations each, window radius {cfg['window']}, S=3",
             "config_index": cfg["index"], "images": cfg["batch"], "M": cfg["M"], "N": cfg["N"],
             "iterations_per_step": cfg["K"], "window": cfg["window"], "S": 3,
+            "phi_solver": ["fft (Eq. 31-33)", "aos (P:427)"][cfg["phi_solver"]],
             "parallelism": {"c3": f"batch-shard x{ngpu} (images split across GPUs, no collective in the loop)",
                             "c5": (f"slab x{ngpu} (row slabs; NCCL halo send/recv + all-to-all spectrum transpose)"
                                    if ngpu > 1 else "single GPU, whole image")}.get(
@@ -227,6 +232,8 @@ def main():
         mode = "slab"
     else:
         mode = "replica" if world > 1 else "single"
+    if mode == "slab" and cfg["phi_solver"]:
+        raise SystemExit("--phi-solver aos is for whole-image contexts (slab mode uses the FFT solve)")
     M, N, K = cfg["M"], cfg["N"], cfg["K"]
     if mode == "batch-shard":
         s0, s1 = shard(B, world, rank)
@@ -250,7 +257,8 @@ def main():
         rows = slice(rank * M // world, (rank + 1) * M // world)
         data["image"] = np.ascontiguousarray(data["image"][:, rows])
         data["phi0"] = np.ascontiguousarray(data["phi0"][:, rows])
-    sv = Solver(M, N, nb, window=p["window"], device=local, stream=stream, **{k: p[k] for k in keys}, **extra)
+    sv = Solver(M, N, nb, window=p["window"], device=local, stream=stream, phi_solver=cfg["phi_solver"],
+                **{k: p[k] for k in keys}, **extra)
     img_d = torch.from_numpy(data["image"]).to(dev)
     phi0_d = torch.from_numpy(data["phi0"]).to(dev)
     out_d = torch.empty_like(phi0_d)

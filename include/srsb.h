@@ -73,7 +73,10 @@ typedef struct {
     int   w_mode;              /* sr_wmode */
     int   w_iters;             /* fixed-point sweeps r for SR_W_FIXED_POINT (Eq. 38-39), >= 1 */
     float b_max;               /* guard: |b| > b_max latches SR_ERR_NONFINITE (SPEC S:366 uses 50); <= 0 off */
+    int   phi_solver;          /* sr_phi_solver: FFT solve of Eq. (31)-(33) (default) or the AOS variant of P:427 */
 } sr_sb_params;
+
+typedef enum { SR_PHI_FFT = 0, SR_PHI_AOS = 1 } sr_phi_solver;   /* AOS: whole-image contexts only */
 
 typedef struct sr_sb_ctx sr_sb_ctx;
 
@@ -147,11 +150,12 @@ sr_status sr_sb_debug_wb(sr_sb_ctx* ctx);
 
 /* Kernel classes of the hot path, in launch order within a sweep / iteration. */
 typedef enum { SR_K_RHS = 0, SR_K_ROWS_R2C = 1, SR_K_COLS_SOLVE = 2, SR_K_ROWS_C2R = 3, SR_K_WB = 4,
-               SR_K_NCLASSES = 5 } sr_kernel_class;
+               SR_K_AOS_VERT = 5, SR_K_AOS_HORIZ = 6,   /* phi_solver = SR_PHI_AOS replaces classes 1-3 */
+               SR_K_NCLASSES = 7 } sr_kernel_class;
 
 /* Diagnostics: run K outer iterations WITHOUT the CUDA graph, bracketing every launch with CUDA
  * events on the context's work stream, and return per kernel class (sr_kernel_class) the summed
- * device time in ms (ms_out[5]) and the number of launches (launches_out[5]).  Synchronizes the
+ * device time in ms (ms_out[SR_K_NCLASSES]) and the number of launches (launches_out[SR_K_NCLASSES]).  Synchronizes the
  * host.  Advances the state exactly like sr_sb_iterate(ctx, K). */
 sr_status sr_sb_profile(sr_sb_ctx* ctx, int K, float* ms_out, int* launches_out);
 

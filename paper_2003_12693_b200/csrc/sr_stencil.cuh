@@ -181,6 +181,7 @@ struct StencilArgs {
     int w_proj;        // 0 ball, 1 sphere, 2 none
     float b_max;
     int tiles_x, tiles_y, ntiles;   // tiles per row, per column, total (x batch)
+    int aos;           // 1: emit the full RHS F (AOS phi solver, NEXT-4); 0: the increment D = F - A psi
     double* stats;     // NEXT-1 monitor: per image [E_g, E_a, E_r, E_pen, ...] accumulated by k_wb; null = off
     int stats_stride;  // doubles per image in stats
 };
@@ -443,8 +444,8 @@ __device__ __forceinline__ void rhs_tile(float4* __restrict__ U, const float* __
             const float wv = w1_[c] * v[i][c].x + w2_[c] * v[i][c].y;
             const RegVals rv = reg_all<LEQ>(ps, a.reg);
             const float t = -a.gamma * g_[c] * wn * rv.dp + a.alpha * g_[c] * rv.d + 2.f * a.beta * rv.hp * wv +
-                            a.mu * (dv + lap);
-            out[c] = a.tau * t;
+                            a.mu * dv;
+            out[c] = a.aos ? ps + a.tau * t : a.tau * (t + a.mu * lap);
         }
         stv<CT>(Do + o, out);
 #pragma unroll

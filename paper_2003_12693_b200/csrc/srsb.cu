@@ -21,6 +21,7 @@
 #include "../../include/srsb.h"
 #include "sr_kernels.h"
 #include "sr_setup.cuh"
+#include "sr_aos.cuh"
 
 using namespace srsb;
 
@@ -87,6 +88,8 @@ struct sr_sb_ctx {
     int stats_stride = 0;
     float* prev_phi = nullptr;     // phi at the previous convergence check (sr_sb_iterate_until)
     double last_change = -1.0;     // outer relative change measured at the last check
+    // NEXT-4 AOS phi solver: LR factors of (I - 2 tau mu A) along columns (M) and rows (N)
+    float *aos_cpM = nullptr, *aos_rM = nullptr, *aos_cpN = nullptr, *aos_rN = nullptr;
     double* conv = nullptr;        // [batch][2] sums of the outer change
     // sr_sb_profile
     bool prof = false;
@@ -145,6 +148,8 @@ sr_status validate(const sr_sb_params* p, std::string& msg) {
     if (p->w_mode != SR_W_THRESHOLD && p->w_mode != SR_W_FIXED_POINT) { msg = "bad w_mode"; return SR_ERR_ARG; }
     if (p->w_mode == SR_W_FIXED_POINT && p->w_iters < 1) { msg = "w_iters must be >= 1"; return SR_ERR_ARG; }
     if (p->phi_clip < 0.f) { msg = "phi_clip must be >= 0"; return SR_ERR_ARG; }
+    if (p->phi_solver != SR_PHI_FFT && p->phi_solver != SR_PHI_AOS) { msg = "bad phi_solver"; return SR_ERR_ARG; }
+    if (p->phi_solver == SR_PHI_AOS && p->N > 8192) { msg = "AOS rows are staged in shared memory: N <= 8192"; return SR_ERR_ARG; }
     return SR_OK;
 }
 
@@ -259,6 +264,7 @@ sr_status configure(sr_sb_ctx* c) {
     a.gamma_mu = p.gamma / p.mu;
     a.w_proj = p.w_proj;
     a.b_max = p.b_max;
+    a.aos = p.phi_solver == SR_PHI_AOS ? 1 : 0;
     // opt-in shared memory above 48 KB
     CK(cudaFuncSetAttribute((const void*)c->rfwd, cudaFuncAttributeMaxDynamicSharedMemorySize, c->rsmem));
     CK(cudaFuncSetAttribute((const void*)c->rinv, cudaFuncAttributeMaxDynamicSharedMemorySize, c->rsmem));
@@ -268,6 +274,9 @@ sr_status configure(sr_sb_ctx* c) {
         for (int u = 0; u < 2; u++)
             CK(cudaFuncSetAttribute((const void*)c->wb[m][u], cudaFuncAttributeMaxDynamicSharedMemorySize, c->ssmem));
     CK(cudaFuncSetAttribute((const void*)c->wb_mon, cudaFuncAttributeMaxDynamicSharedMemorySize, c->ssmem));
+    if (p.phi_solver == SR_PHI_AOS)
+        CK(cudaFuncSetAttribute((const void*)k_aos_horiz, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)aos_horiz_smem(N)));
     c->sgrid = dim3(a.tiles_x, a.tiles_y, B);
     return SR_OK;
 }
@@ -287,6 +296,28 @@ sr_status make_tables(sr_sb_ctx* c) {
     CK(cudaMemcpyAsync(c->twR, twR.data(), H * sizeof(float2), cudaMemcpyHostToDevice, c->s));
     CK(cudaMemcpyAsync(c->cM, cM.data(), M * sizeof(float), cudaMemcpyHostToDevice, c->s));
     CK(cudaMemcpyAsync(c->cN, cN.data(), (H + 1) * sizeof(float), cudaMemcpyHostToDevice, c->s));
+    if (c->p.phi_solver == SR_PHI_AOS) {   // LR factors once, fp64 -> fp32
+        auto factors = [&](int n, std::vector<float>& cp, std::vector<float>& r) {
+            const double cc = 2.0 * (double)c->p.tau * (double)c->p.mu, a = -cc;
+            cp.assign(n, 0.f);
+            r.assign(n, 0.f);
+            double cprev = 0.0;
+            for (int i = 0; i < n; i++) {
+                const double diag = (i == 0 || i == n - 1) ? 1.0 + cc : 1.0 + 2.0 * cc;
+                const double d = diag - (i > 0 ? a * cprev : 0.0);
+                r[i] = (float)(1.0 / d);
+                cprev = a / d;
+                cp[i] = (float)cprev;
+            }
+        };
+        std::vector<float> cpM, rM, cpN, rN;
+        factors(M, cpM, rM);
+        factors(N, cpN, rN);
+        CK(cudaMemcpyAsync(c->aos_cpM, cpM.data(), M * 4, cudaMemcpyHostToDevice, c->s));
+        CK(cudaMemcpyAsync(c->aos_rM, rM.data(), M * 4, cudaMemcpyHostToDevice, c->s));
+        CK(cudaMemcpyAsync(c->aos_cpN, cpN.data(), N * 4, cudaMemcpyHostToDevice, c->s));
+        CK(cudaMemcpyAsync(c->aos_rN, rN.data(), N * 4, cudaMemcpyHostToDevice, c->s));
+    }
     CK(cudaStreamSynchronize(c->s));
     return SR_OK;
 }
@@ -444,13 +475,48 @@ sr_status alltoall(std::vector<sr_sb_ctx*>& m, bool fwd) {
 }
 
 // ------------------------------------------------------------------ the iteration
+// NEXT-4: phi = 1/2 [(I - c A_1)^-1 + (I - c A_2)^-1] F with F the full RHS (AOS)
+void enq_aos(sr_sb_ctx* c, const float* F, float* out, float clip) {
+    AosArgs q;
+    q.M = c->Ml;
+    q.N = c->p.N;
+    q.plane = c->pitch;
+    q.a = -2.f * c->p.tau * c->p.mu;
+    q.clip = clip;
+    float* Y = c->w[c->wcur ^ 1];          // scratch: the w ping-pong target is free during the sweeps
+    float* Xv = Y + c->pitch * c->p.batch;  // its second half (the [B][2] planes hold 2 B planes)
+    prof_begin(c);
+    if (q.M <= AOS_VREG_MAXM) {
+        const int L = q.M < 32 ? q.M : 32, CH = q.M / L;
+        const int CW = std::min(std::min(32, AOS_VT / CH), q.N);
+        const dim3 grd(q.N / CW, c->p.batch), blk(CW, CH);
+        const size_t sm = 4 * (size_t)CH * CW * sizeof(float);
+        if (L == 8) k_aos_vert_reg<8><<<grd, blk, sm, c->s>>>(F, Xv, c->aos_cpM, c->aos_rM, q);
+        else if (L == 16) k_aos_vert_reg<16><<<grd, blk, sm, c->s>>>(F, Xv, c->aos_cpM, c->aos_rM, q);
+        else k_aos_vert_reg<32><<<grd, blk, sm, c->s>>>(F, Xv, c->aos_cpM, c->aos_rM, q);
+    } else {
+        k_aos_vert<<<dim3((q.N + 127) / 128, c->p.batch), 128, 0, c->s>>>(F, Y, Xv, c->aos_cpM, c->aos_rM, q);
+    }
+    prof_end(c, SR_K_AOS_VERT);
+    prof_begin(c);
+    const int wpb = aos_horiz_wpb(q.N);
+    k_aos_horiz<<<dim3((q.M + wpb - 1) / wpb, c->p.batch), 32 * wpb, aos_horiz_smem(q.N), c->s>>>(
+        F, Xv, out, c->aos_cpN, c->aos_rN, q);
+    prof_end(c, SR_K_AOS_HORIZ);
+}
+
 sr_status enq_iteration(sr_sb_ctx* c) {   // whole-image context
     if (c->stats) cudaMemsetAsync(c->stats, 0, sizeof(double) * c->stats_stride * c->p.batch, c->s);
     for (int s = 0; s < c->p.S; s++) {
         enq_rhs(c, c->F);
-        enq_r2c(c, c->F);
-        enq_cols(c);
-        enq_c2r(c, c->phi, (s == c->p.S - 1) ? c->p.phi_clip : 0.f, 1, s);
+        const float clip = (s == c->p.S - 1) ? c->p.phi_clip : 0.f;
+        if (c->p.phi_solver == SR_PHI_AOS) {
+            enq_aos(c, c->F, c->phi, clip);
+        } else {
+            enq_r2c(c, c->F);
+            enq_cols(c);
+            enq_c2r(c, c->phi, clip, 1, s);
+        }
     }
     const int passes = c->p.w_mode == SR_W_FIXED_POINT ? c->p.w_iters : 1;
     for (int r = 0; r < passes; r++) enq_wb_pass(c, r == passes - 1);
@@ -564,6 +630,9 @@ sr_status create_one(const sr_sb_params* p, int device, cudaStream_t stream, int
          alloc((void**)&c->cM, p->M * sizeof(float)) && alloc((void**)&c->cN, (p->N / 2 + 1) * sizeof(float)) &&
          alloc((void**)&c->flag, sizeof(int));
     if (ok && c->slab) ok = alloc((void**)&c->spec_cols, nspec * sizeof(float2));
+    if (ok && p->phi_solver == SR_PHI_AOS)
+        ok = alloc((void**)&c->aos_cpM, p->M * 4) && alloc((void**)&c->aos_rM, p->M * 4) &&
+             alloc((void**)&c->aos_cpN, p->N * 4) && alloc((void**)&c->aos_rN, p->N * 4);
     if (!ok) { g_create_err = "device allocation failed"; sr_sb_destroy(c); return SR_ERR_OOM; }
     const size_t off = (size_t)c->gh * p->N;
     c->phi = c->phi_base + off;
@@ -600,6 +669,7 @@ sr_status check_device(int device) {
 sr_status validate_slab(const sr_sb_params* p, int nranks, std::string& msg) {
     if (nranks < 1 || !is_pow2(nranks)) { msg = "nranks must be a power of two"; return SR_ERR_ARG; }
     if (p->batch != 1) { msg = "slab mode decomposes one image: batch must be 1"; return SR_ERR_ARG; }
+    if (p->phi_solver != SR_PHI_FFT) { msg = "slab mode uses the FFT phi solver"; return SR_ERR_ARG; }
     const int Ml = p->M / nranks, gh = ghost_rows(*p);
     if (Ml < 8 || Ml < gh) { msg = "too many slabs: local rows must be >= 8 and >= the ghost rows"; return SR_ERR_SHAPE; }
     if ((p->N / 2) % nranks != 0) { msg = "N/2 must be divisible by nranks"; return SR_ERR_SHAPE; }
@@ -693,6 +763,7 @@ void sr_sb_default_params(sr_sb_params* p, int M, int N, int batch, int window) 
     p->w_mode = SR_W_THRESHOLD;
     p->w_iters = 1;
     p->b_max = 50.f;
+    p->phi_solver = SR_PHI_FFT;
 }
 
 sr_status sr_sb_create(const sr_sb_params* p, int device, void* stream, sr_sb_ctx** out) {
@@ -927,11 +998,16 @@ sr_status sr_sb_debug_solve(sr_sb_ctx* c, const float* F, float* phi_out) {
     RET(begin(c));
     RET(copy_planes(c, c->F, F, c->p.batch, true));
     // solve into F's own buffer is not allowed (rows read F while c2r writes); use w[1] as output
-    float* tmp = c->w[c->wcur ^ 1];
-    enq_r2c(c, c->F);
-    enq_cols(c);
-    enq_c2r(c, tmp, 0.f, 0);
-    RET(copy_planes(c, tmp, phi_out, c->p.batch, false));
+    if (c->p.phi_solver == SR_PHI_AOS) {   // AOS: F is the full RHS; k_aos_horiz may write in place
+        enq_aos(c, c->F, c->F, 0.f);
+        RET(copy_planes(c, c->F, phi_out, c->p.batch, false));
+    } else {
+        float* tmp = c->w[c->wcur ^ 1];
+        enq_r2c(c, c->F);
+        enq_cols(c);
+        enq_c2r(c, tmp, 0.f, 0);
+        RET(copy_planes(c, tmp, phi_out, c->p.batch, false));
+    }
     RET(end(c));
     return SR_OK;
 }
@@ -1076,7 +1152,8 @@ void sr_sb_destroy(sr_sb_ctx* c) {
     if (c->graph) cudaGraphExecDestroy(c->graph);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     void* ptrs[] = {c->phi_base, c->F_base, c->w_base[0], c->w_base[1], c->b_base, c->g_base, c->spec,
-                    c->spec_cols, c->twH, c->twM, c->twR, c->cM, c->cN, c->flag, c->stats, c->prev_phi, c->conv};
+                    c->spec_cols, c->twH, c->twM, c->twR, c->cM, c->cN, c->flag, c->stats, c->prev_phi, c->conv,
+                    c->aos_cpM, c->aos_rM, c->aos_cpN, c->aos_rN};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (c->ev_in) cudaEventDestroy(c->ev_in);

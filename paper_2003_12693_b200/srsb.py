@@ -28,7 +28,7 @@ EXPORTS = ["sr_sb_default_params", "sr_sb_create", "sr_sb_set_image", "sr_sb_ite
            "sr_sb_last_error", "sr_sb_abi_version", "sr_sb_profile", "sr_sb_create_slab_group",
            "sr_sb_nccl_unique_id", "sr_sb_create_slab_nccl", "sr_sb_local_rows", "sr_sb_set_monitor",
            "sr_sb_get_monitor", "sr_sb_iterate_until", "sr_sb_last_change"]
-KERNEL_CLASSES = ["rhs", "rows_r2c", "cols_solve", "rows_c2r", "wb"]
+KERNEL_CLASSES = ["rhs", "rows_r2c", "cols_solve", "rows_c2r", "wb", "aos_vert", "aos_horiz"]   # sr_kernel_class
 
 
 class SrsbError(RuntimeError):
@@ -44,7 +44,7 @@ class Params(C.Structure):
                 ("epsilon", C.c_float), ("l", C.c_float), ("d", C.c_float), ("window", C.c_int),
                 ("window_shape", C.c_int), ("tau", C.c_float), ("S", C.c_int), ("rho", C.c_float),
                 ("sigma", C.c_float), ("s", C.c_int), ("phi_clip", C.c_float), ("w_proj", C.c_int),
-                ("w_mode", C.c_int), ("w_iters", C.c_int), ("b_max", C.c_float)]
+                ("w_mode", C.c_int), ("w_iters", C.c_int), ("b_max", C.c_float), ("phi_solver", C.c_int)]
 
 
 _lib = None
@@ -227,10 +227,10 @@ class Solver:
 
     def profile(self, K):
         """sr_sb_profile: per kernel class {name: (ms_total, launches)} over K ungraphed iterations."""
-        ms = (C.c_float * 5)()
-        n = (C.c_int * 5)()
+        ms = (C.c_float * len(KERNEL_CLASSES))()
+        n = (C.c_int * len(KERNEL_CLASSES))()
         self._check(lib().sr_sb_profile(self._ctx, int(K), ms, n))
-        return {name: (float(ms[i]), int(n[i])) for i, name in enumerate(KERNEL_CLASSES)}
+        return {name: (float(ms[i]), int(n[i])) for i, name in enumerate(KERNEL_CLASSES) if n[i]}
 
     def set_monitor(self, enable=True):
         self._check(lib().sr_sb_set_monitor(self._ctx, int(bool(enable))))

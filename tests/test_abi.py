@@ -58,6 +58,15 @@ def test_params_struct_matches_header(srsb):
     assert mirror == fields
 
 
+def test_kernel_classes_match_header(srsb):
+    hdr = open(os.path.join(ROOT, "include", "srsb.h")).read()
+    body = re.search(r"typedef enum \{\s*(SR_K_RHS.*?)\} sr_kernel_class;", hdr, re.S).group(1)
+    names = re.findall(r"SR_K_(\w+) = (\d+)", body)
+    classes = [n.lower() for n, v in names if n != "NCLASSES"]
+    assert classes == srsb.KERNEL_CLASSES
+    assert dict(names)["NCLASSES"] == str(len(classes))
+
+
 def test_default_params_are_the_design_readings(srsb):
     p = srsb.default_params(128, 128, 1, 3)
     assert (p["gamma"], p["alpha"], p["mu"], p["S"]) == (1.0, 4.0, 8.0, 3)
@@ -74,7 +83,8 @@ def test_default_params_are_the_design_readings(srsb):
 @pytest.mark.parametrize("field,value,status", [
     ("M", 100, -2), ("N", 16384, -2), ("M", 4, -2), ("batch", 0, -2), ("S", 0, -1), ("s", 3, -1),
     ("window", 9, -1), ("window", -1, -1), ("mu", 0.0, -1), ("epsilon", 0.0, -1), ("window_shape", 2, -1),
-    ("w_proj", 3, -1), ("w_mode", 2, -1), ("sigma", 3.0, -1), ("phi_clip", -1.0, -1)])
+    ("w_proj", 3, -1), ("w_mode", 2, -1), ("sigma", 3.0, -1), ("phi_clip", -1.0, -1),
+    ("phi_solver", 2, -1), ("phi_solver", -1, -1)])
 def test_create_validates_before_device(srsb, field, value, status):
     p = srsb.Params()
     srsb.lib().sr_sb_default_params(C.byref(p), 64, 64, 1, 3)

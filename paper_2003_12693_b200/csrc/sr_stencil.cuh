@@ -16,6 +16,7 @@
 // row half-width -- an exact regrouping of the window sum (different rounding order).
 #pragma once
 #include <cuda_runtime.h>
+#include "sr_tma.cuh"
 
 namespace srsb {
 
@@ -181,6 +182,7 @@ struct StencilArgs {
     int w_proj;        // 0 ball, 1 sphere, 2 none
     float b_max;
     int tiles_x, tiles_y, ntiles;   // tiles per row, per column, total (x batch)
+    int gh;            // ghost rows above each plane (TMA coordinates address the allocation rows)
     int aos;           // 1: emit the full RHS F (AOS phi solver, NEXT-4); 0: the increment D = F - A psi
     double* stats;     // NEXT-1 monitor: per image [E_g, E_a, E_r, E_pen, ...] accumulated by k_wb; null = off
     int stats_stride;  // doubles per image in stats
@@ -306,15 +308,15 @@ __device__ __forceinline__ void stage_u(float4* __restrict__ U, const float* __r
 
 // v for the thread's RT x CT block (tile-local rows r0.., cols c0..) from the staged u, in packed
 // f32x2 arithmetic (both channels per instruction); conflict-free LDS.128 row reads.
-template <int R, int SHAPE>
+template <int R, int SHAPE, int RT = ST_RT>
 __device__ __forceinline__ void window_block(const float4* __restrict__ U, int r0, int c0, const float* e,
-                                             float2 (&v)[ST_RT][ST_CT]) {
+                                             float2 (&v)[RT][ST_CT]) {
     using TG = TileGeom<R>;
     constexpr int OFF = (TG::RA - R) & 1;                 // first needed float2 is odd -> load one earlier
     constexpr int NA = ST_CT + 2 * R + OFF;               // float2 values loaded per halo row
     constexpr int NC = (NA + 1) / 2;                      // chunks loaded per halo row
 #pragma unroll
-    for (int i = 0; i < ST_RT; i++)
+    for (int i = 0; i < RT; i++)
 #pragma unroll
         for (int c = 0; c < ST_CT; c++) v[i][c] = make_float2(0.f, 0.f);
     float2 ew[R + 1];
@@ -322,7 +324,7 @@ __device__ __forceinline__ void window_block(const float4* __restrict__ U, int r
     for (int q = 0; q <= R; q++) ew[q] = make_float2(e[q], e[q]);
     const int chunk0 = (c0 + TG::RA - R - OFF) >> 1;
 #pragma unroll
-    for (int rr = 0; rr < ST_RT + 2 * R; rr++) {
+    for (int rr = 0; rr < RT + 2 * R; rr++) {
         float2 a[2 * NC];
         const float4* row = U + (r0 + rr) * TG::LDC;
 #pragma unroll
@@ -345,7 +347,7 @@ __device__ __forceinline__ void window_block(const float4* __restrict__ U, int r
             }
         }
 #pragma unroll
-        for (int i = 0; i < ST_RT; i++) {
+        for (int i = 0; i < RT; i++) {
             const int p = rr - R - i;   // row offset of this halo row w.r.t. output row i
             if (p >= -R && p <= R) {
                 const int ap = p < 0 ? -p : p;
@@ -590,6 +592,149 @@ __global__ void __launch_bounds__(32 * ST_BY, ST_MINB) k_rhs(const float* __rest
                                                     float* __restrict__ D, StencilArgs a) {
     extern __shared__ float4 U[];
     rhs_tile<R, SHAPE, LEQ>(U, phi, w, bv, g, D, a, blockIdx.z, blockIdx.y, blockIdx.x);
+}
+
+// ------------------------------------------------------------------ TMA-staged RHS (k_rhs_tma)
+// Same arithmetic as rhs_tile, different data movement: one elected thread issues six TMA box
+// loads (phi and w1, w2 with the window halo; b1, b2 with the one-row / one-column divergence
+// halo; g) completing on one mbarrier, so a CTA has its whole 32 x 64 tile (~60 KB) in flight at
+// once instead of a few loads per thread; u = h(phi) w, the Laplacian, the divergence and every
+// pointwise field then come from shared memory.  Boxes address the allocation rows (ghost rows
+// included); rows outside the image are masked in the u staging exactly as in stage_u, columns
+// outside are zero-filled by the TMA unit (w = 0 -> u = 0, reading Q5).
+struct RhsMaps {
+    CUtensorMap phi, w, b, g;   // phi / w: box PW x PH; b: BW x BH; g: TW x TH (TmaGeom)
+};
+
+constexpr int TMA_TH = 32;                                            // tile rows of the TMA kernels
+constexpr int tma_hr(int R) { return R > 1 ? R : 1; }                 // box row halo (the Laplacian needs 1)
+// box column halo: >= the u halo RA and >= 1 (Laplacian), rounded to 4 columns so every box row is a
+// multiple of 32 bytes (box rows of 272 / 304 bytes faulted with an illegal instruction on B200)
+constexpr int tma_ca(int R) { return ((((R + 1) & ~1) > 1 ? ((R + 1) & ~1) : 1) + 3) & ~3; }
+constexpr int tma_pw(int R) { return ST_TW + 2 * tma_ca(R); }          // phi / w box width
+constexpr int tma_ph(int R) { return TMA_TH + 2 * tma_hr(R); }         // phi / w box height
+
+template <int R>
+struct TmaGeom {
+    static constexpr int TH = TMA_TH, TW = ST_TW, RT = 4;   // 8 thread rows x 4 rows, 32 x 2 columns
+    static constexpr int RA = TileGeom<R>::RA;           // u halo columns (even)
+    static constexpr int HR = tma_hr(R), CA = tma_ca(R);
+    static constexpr int PW = tma_pw(R), PH = tma_ph(R);
+    static constexpr int BW = TW + 8, BH = TH + 1;       // b box: columns col0-4.., rows row0-1.. (32-byte rows)
+    static constexpr int UROWS = TH + 2 * R, LDC = TileGeom<R>::LDC, UCH = TileGeom<R>::CH;
+    static constexpr int al(int x) { return (x + 127) & ~127; }
+    static constexpr int S_P = al(PW * PH * 4), S_B = al(BW * BH * 4), S_G = al(TW * TH * 4);
+    static constexpr int O_P = 0, O_W1 = S_P, O_W2 = 2 * S_P, O_B1 = 3 * S_P, O_B2 = O_B1 + S_B;
+    static constexpr int O_G = O_B2 + S_B, O_U = O_G + S_G, O_BAR = O_U + LDC * UROWS * 16;
+    static constexpr int BYTES = O_BAR + 16 + 128;       // + alignment slack of the dynamic base
+    static constexpr uint32_t TX = (uint32_t)(3 * PW * PH + 2 * BW * BH + TW * TH) * 4;
+};
+
+template <int R, int SHAPE, bool LEQ>
+__global__ void __launch_bounds__(256, 2) k_rhs_tma(const __grid_constant__ RhsMaps maps,
+                                                    const float* __restrict__ phi, float* __restrict__ D,
+                                                    StencilArgs a) {
+    using G = TmaGeom<R>;
+    extern __shared__ unsigned char sm_raw[];
+    unsigned char* sm = sm_raw + ((128 - (smem_u32(sm_raw) & 127)) & 127);
+    float* Ps = reinterpret_cast<float*>(sm + G::O_P);
+    float* W1s = reinterpret_cast<float*>(sm + G::O_W1);
+    float* W2s = reinterpret_cast<float*>(sm + G::O_W2);
+    float* B1s = reinterpret_cast<float*>(sm + G::O_B1);
+    float* B2s = reinterpret_cast<float*>(sm + G::O_B2);
+    float* Gs = reinterpret_cast<float*>(sm + G::O_G);
+    float4* U = reinterpret_cast<float4*>(sm + G::O_U);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + G::O_BAR);
+    const int img = blockIdx.z, row0 = blockIdx.y * G::TH, col0 = blockIdx.x * G::TW;
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    if (tid == 0) mbar_init(bar, 1);
+    __syncthreads();
+    if (tid == 0) {
+        mbar_expect_tx(bar, G::TX);
+        const int ar = a.gh + row0;   // allocation row of local row row0
+        tma_load_3d(Ps, &maps.phi, bar, col0 - G::CA, ar - G::HR, img);
+        tma_load_3d(W1s, &maps.w, bar, col0 - G::CA, ar - G::HR, 2 * img);
+        tma_load_3d(W2s, &maps.w, bar, col0 - G::CA, ar - G::HR, 2 * img + 1);
+        tma_load_3d(B1s, &maps.b, bar, col0 - 4, ar - 1, 2 * img);
+        tma_load_3d(B2s, &maps.b, bar, col0 - 4, ar - 1, 2 * img + 1);
+        tma_load_3d(Gs, &maps.g, bar, col0, ar, img);
+    }
+    mbar_wait(bar, 0);
+    // u = h(phi) w over the tile + R halo, as 16-byte chunks (2 px x 2 channels) in TileGeom's layout
+    for (int k = tid; k < G::UROWS * G::UCH; k += 256) {
+        const int r = k / G::UCH, f = k - r * G::UCH;
+        const int gi = row0 - R + r;
+        float4 A = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (gi + a.row_off >= 0 && gi + a.row_off < a.Mg) {
+            const int o = (r + G::HR - R) * G::PW + (G::CA - G::RA) + 2 * f;
+            const float2 P = *reinterpret_cast<const float2*>(Ps + o);
+            const float2 X = *reinterpret_cast<const float2*>(W1s + o);
+            const float2 Y = *reinterpret_cast<const float2*>(W2s + o);
+            const float h0 = reg_h<LEQ>(P.x, a.reg), h1 = reg_h<LEQ>(P.y, a.reg);
+            A = make_float4(h0 * X.x, h0 * Y.x, h1 * X.y, h1 * Y.y);
+        }
+        U[r * G::LDC + swz(f)] = A;
+    }
+    __syncthreads();
+    const int r0 = threadIdx.y * G::RT, c0 = threadIdx.x * ST_CT;
+    const int M = a.M, N = a.N, gj = col0 + c0;
+    if (gj >= N || row0 + r0 >= M) return;
+    float2 v[G::RT][ST_CT];
+    window_block<R, SHAPE, G::RT>(U, r0, c0, a.e, v);
+    constexpr int CT = ST_CT;
+    const float* ph = phi + img * a.plane;
+    float* Do = D + img * a.plane;
+#pragma unroll
+    for (int i = 0; i < G::RT; i++) {
+        const int tr = r0 + i, gi = row0 + tr;
+        if (gi >= M) break;
+        const int gig = gi + a.row_off;
+        const float* prow = Ps + (G::HR + tr) * G::PW + G::CA + c0;
+        const float* w1r = W1s + (G::HR + tr) * G::PW + G::CA + c0;
+        const float* w2r = W2s + (G::HR + tr) * G::PW + G::CA + c0;
+        const float* b1r = B1s + (1 + tr) * G::BW + 4 + c0;
+        const float* b2r = B2s + (1 + tr) * G::BW + 4 + c0;
+        const float2 P = *reinterpret_cast<const float2*>(prow);
+        float2 Pu = *reinterpret_cast<const float2*>(prow - G::PW);
+        float2 Pd = *reinterpret_cast<const float2*>(prow + G::PW);
+        if (!a.slab) {   // periodic rows of Eq. (32) wrap in-kernel for a whole image
+            if (gi == 0) Pu = __ldg(reinterpret_cast<const float2*>(ph + (long long)(M - 1) * N + gj));
+            if (gi == M - 1) Pd = __ldg(reinterpret_cast<const float2*>(ph + gj));
+        }
+        const float pl = gj == 0 ? __ldg(ph + (long long)gi * N + N - 1) : prow[-1];
+        const float pr = gj + CT == N ? __ldg(ph + (long long)gi * N) : prow[CT];
+        const float2 W1 = *reinterpret_cast<const float2*>(w1r), W2 = *reinterpret_cast<const float2*>(w2r);
+        const float2 W1u = *reinterpret_cast<const float2*>(w1r - G::PW);
+        const float2 B1 = *reinterpret_cast<const float2*>(b1r), B2 = *reinterpret_cast<const float2*>(b2r);
+        const float2 B1u = *reinterpret_cast<const float2*>(b1r - G::BW);
+        const float2 Gv = *reinterpret_cast<const float2*>(Gs + tr * G::TW + c0);
+        const float c2l0 = b2r[-1] - w2r[-1];   // (b2 - w2) at column gj - 1 (unused at gj = 0)
+        const float ps_[CT] = {P.x, P.y}, pu_[CT] = {Pu.x, Pu.y}, pd_[CT] = {Pd.x, Pd.y};
+        const float w1_[CT] = {W1.x, W1.y}, w2_[CT] = {W2.x, W2.y}, g_[CT] = {Gv.x, Gv.y};
+        const float c1_[CT] = {B1.x - W1.x, B1.y - W1.y}, c1u_[CT] = {B1u.x - W1u.x, B1u.y - W1u.y};
+        const float c2_[CT] = {B2.x - W2.x, B2.y - W2.y};
+        float out[CT];
+#pragma unroll
+        for (int c = 0; c < CT; c++) {
+            const int j = gj + c;
+            float dv = 0.f;
+            if (gig < a.Mg - 1) dv += c1_[c];
+            if (gig > 0) dv -= c1u_[c];
+            if (j < N - 1) dv += c2_[c];
+            if (j > 0) dv -= (c == 0 ? c2l0 : c2_[c - 1]);
+            const float ps = ps_[c];
+            const float left = c > 0 ? ps_[c > 0 ? c - 1 : 0] : pl;
+            const float right = c < CT - 1 ? ps_[c < CT - 1 ? c + 1 : 0] : pr;
+            const float lap = ((pu_[c] - ps) + (pd_[c] - ps)) + ((left - ps) + (right - ps));
+            const float wn = sqrt_approx(w1_[c] * w1_[c] + w2_[c] * w2_[c]);
+            const float wv = w1_[c] * v[i][c].x + w2_[c] * v[i][c].y;
+            const RegVals rv = reg_all<LEQ>(ps, a.reg);
+            const float t = -a.gamma * g_[c] * wn * rv.dp + a.alpha * g_[c] * rv.d + 2.f * a.beta * rv.hp * wv +
+                            a.mu * dv;
+            out[c] = a.aos ? ps + a.tau * t : a.tau * (t + a.mu * lap);
+        }
+        stv<CT>(Do + (long long)gi * N + gj, out);
+    }
 }
 
 // MON: the NEXT-1 monitor variant (Eq. 22 energy partial sums), used only when monitoring is on

@@ -20,6 +20,7 @@
 
 #include "../../include/srsb.h"
 #include "sr_kernels.h"
+#include <cudaTypedefs.h>
 #include "sr_setup.cuh"
 #include "sr_aos.cuh"
 
@@ -76,6 +77,10 @@ struct sr_sb_ctx {
     RowInvKernel rinv = nullptr;
     ColKernel cols = nullptr;
     RhsKernel rhs = nullptr;
+    RhsTmaKernel rhs_tma = nullptr;   // TMA-staged RHS (default; SRSB_TMA=0 selects k_rhs)
+    RhsMaps tmaps[2];                 // tensor maps, per w ping-pong buffer
+    dim3 tgrid;
+    int tsmem = 0;
     WbKernel wb[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
     WbKernel wb_mon = nullptr;     // monitor variant (threshold mode, last pass)
     FftRowArgs ra{};
@@ -158,6 +163,26 @@ int ghost_rows(const sr_sb_params& p) {
     int gh = p.window > 1 ? p.window : 1;       // window halo, Laplacian / gradient / divergence
     if (rblur + 1 > gh) gh = rblur + 1;          // edge indicator: blur radius + central difference
     return gh;
+}
+
+// 3-D tiled tensor map over a field allocation: {N columns, rows per plane, planes}, fp32, box
+// {bw, bh, 1}; out-of-bounds boxes are zero-filled.
+bool encode_map3d(CUtensorMap* m, float* base, int N, int rows, int planes, int bw, int bh) {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess || !f)
+            return false;
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }
+    const cuuint64_t dims[3] = {(cuuint64_t)N, (cuuint64_t)rows, (cuuint64_t)planes};
+    const cuuint64_t strides[2] = {(cuuint64_t)N * 4, (cuuint64_t)N * rows * 4};
+    const cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, 1}, es[3] = {1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 sr_status configure(sr_sb_ctx* c) {
@@ -265,6 +290,27 @@ sr_status configure(sr_sb_ctx* c) {
     a.w_proj = p.w_proj;
     a.b_max = p.b_max;
     a.aos = p.phi_solver == SR_PHI_AOS ? 1 : 0;
+    a.gh = c->gh;
+    {   // TMA-staged RHS
+        const char* e = getenv("SRSB_TMA");
+        if (!(e && e[0] == '0') && pick_rhs_tma(p.window, p.window_shape, p.l == p.epsilon, c->rhs_tma, c->tsmem)) {
+            const int R = p.window, rows = Ml + 2 * c->gh;
+            const int pw = tma_pw(R), ph = tma_ph(R);
+            bool mok = true;
+            for (int u = 0; u < 2; u++) {
+                RhsMaps& m = c->tmaps[u];
+                mok = mok && encode_map3d(&m.phi, c->phi_base, N, rows, B, pw, ph) &&
+                      encode_map3d(&m.w, c->w_base[u], N, rows, 2 * B, pw, ph) &&
+                      encode_map3d(&m.b, c->b_base, N, rows, 2 * B, ST_TW + 8, TMA_TH + 1) &&
+                      encode_map3d(&m.g, c->g_base, N, rows, B, ST_TW, TMA_TH);
+            }
+            if (!mok) return fail(c, SR_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+            c->tgrid = dim3(a.tiles_x, (Ml + TMA_TH - 1) / TMA_TH, B);
+            CK(cudaFuncSetAttribute((const void*)c->rhs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, c->tsmem));
+        } else {
+            c->rhs_tma = nullptr;
+        }
+    }
     // opt-in shared memory above 48 KB
     CK(cudaFuncSetAttribute((const void*)c->rfwd, cudaFuncAttributeMaxDynamicSharedMemorySize, c->rsmem));
     CK(cudaFuncSetAttribute((const void*)c->rinv, cudaFuncAttributeMaxDynamicSharedMemorySize, c->rsmem));
@@ -364,7 +410,10 @@ void enq_c2r(sr_sb_ctx* c, float* out, float clip, int accum, int sweep = -1) {
 }
 void enq_rhs(sr_sb_ctx* c, float* F) {
     prof_begin(c);
-    c->rhs<<<c->sgrid, c->sblock, c->ssmem, c->s>>>(c->phi, c->w[c->wcur], c->b, c->g, F, c->sa);
+    if (c->rhs_tma)
+        c->rhs_tma<<<c->tgrid, c->sblock, c->tsmem, c->s>>>(c->tmaps[c->wcur], c->phi, F, c->sa);
+    else
+        c->rhs<<<c->sgrid, c->sblock, c->ssmem, c->s>>>(c->phi, c->w[c->wcur], c->b, c->g, F, c->sa);
     prof_end(c, SR_K_RHS);
 }
 void enq_wb_pass(sr_sb_ctx* c, int last) {

@@ -22,4 +22,13 @@ bool SRSB_CAT(pick_stencil_r, SRSB_R)(int shape, bool leq, RhsKernel& rhs, WbKer
     smem = TileGeom<SRSB_R>::BYTES;
     return true;
 }
+bool SRSB_CAT(pick_rhs_tma_r, SRSB_R)(int shape, bool leq, RhsTmaKernel& k, int& smem) {
+    if (shape == 0 && leq) k = k_rhs_tma<SRSB_R, 0, true>;
+    else if (shape == 0) k = k_rhs_tma<SRSB_R, 0, false>;
+    else if (shape == 1 && leq) k = k_rhs_tma<SRSB_R, 1, true>;
+    else if (shape == 1) k = k_rhs_tma<SRSB_R, 1, false>;
+    else return false;
+    smem = TmaGeom<SRSB_R>::BYTES;
+    return true;
+}
 }  // namespace srsb

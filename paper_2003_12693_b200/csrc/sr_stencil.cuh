@@ -308,7 +308,7 @@ __device__ __forceinline__ void stage_u(float4* __restrict__ U, const float* __r
 
 // v for the thread's RT x CT block (tile-local rows r0.., cols c0..) from the staged u, in packed
 // f32x2 arithmetic (both channels per instruction); conflict-free LDS.128 row reads.
-template <int R, int SHAPE, int RT = ST_RT>
+template <int R, int SHAPE, int RT = ST_RT, int LDC = TileGeom<R>::LDC>
 __device__ __forceinline__ void window_block(const float4* __restrict__ U, int r0, int c0, const float* e,
                                              float2 (&v)[RT][ST_CT]) {
     using TG = TileGeom<R>;
@@ -326,7 +326,7 @@ __device__ __forceinline__ void window_block(const float4* __restrict__ U, int r
 #pragma unroll
     for (int rr = 0; rr < RT + 2 * R; rr++) {
         float2 a[2 * NC];
-        const float4* row = U + (r0 + rr) * TG::LDC;
+        const float4* row = U + (r0 + rr) * LDC;
 #pragma unroll
         for (int k = 0; k < NC; k++) {
             const float4 q4 = row[swz(chunk0 + k)];
@@ -595,11 +595,14 @@ __global__ void __launch_bounds__(32 * ST_BY, ST_MINB) k_rhs(const float* __rest
 }
 
 // ------------------------------------------------------------------ TMA-staged RHS (k_rhs_tma)
-// Same arithmetic as rhs_tile, different data movement: one elected thread issues six TMA box
-// loads (phi and w1, w2 with the window halo; b1, b2 with the one-row / one-column divergence
-// halo; g) completing on one mbarrier, so a CTA has its whole 32 x 64 tile (~60 KB) in flight at
-// once instead of a few loads per thread; u = h(phi) w, the Laplacian, the divergence and every
-// pointwise field then come from shared memory.  Boxes address the allocation rows (ghost rows
+// Same arithmetic as rhs_tile, different data movement.  One elected thread issues TMA box loads
+// completing on mbarriers, so a CTA has a whole box set in flight at once instead of a few loads
+// per thread:
+//   group 1 (bar[0]): phi, w1, w2 over the tile + window halo -> u = h(phi) w staged as chunks;
+//   group 2 (bar[1]): b1, b2 (one-row / one-column divergence halo) and g, loaded into the u
+//                     region once the window sums are in registers (u is dead by then).
+// Reusing the u region keeps the CTA at ~62 KB of shared memory (3 CTAs per SM) while the other
+// resident CTAs cover each CTA's two load waits.  Boxes address the allocation rows (ghost rows
 // included); rows outside the image are masked in the u staging exactly as in stage_u, columns
 // outside are zero-filled by the TMA unit (w = 0 -> u = 0, reading Q5).
 struct RhsMaps {
@@ -613,6 +616,7 @@ constexpr int tma_hr(int R) { return R > 1 ? R : 1; }                 // box row
 constexpr int tma_ca(int R) { return ((((R + 1) & ~1) > 1 ? ((R + 1) & ~1) : 1) + 3) & ~3; }
 constexpr int tma_pw(int R) { return ST_TW + 2 * tma_ca(R); }          // phi / w box width
 constexpr int tma_ph(int R) { return TMA_TH + 2 * tma_hr(R); }         // phi / w box height
+constexpr int TMA_BW = ST_TW + 8, TMA_BH = TMA_TH + 1;                 // b box: columns col0-4.., rows row0-1..
 
 template <int R>
 struct TmaGeom {
@@ -620,18 +624,20 @@ struct TmaGeom {
     static constexpr int RA = TileGeom<R>::RA;           // u halo columns (even)
     static constexpr int HR = tma_hr(R), CA = tma_ca(R);
     static constexpr int PW = tma_pw(R), PH = tma_ph(R);
-    static constexpr int BW = TW + 8, BH = TH + 1;       // b box: columns col0-4.., rows row0-1.. (32-byte rows)
-    static constexpr int UROWS = TH + 2 * R, LDC = TileGeom<R>::LDC, UCH = TileGeom<R>::CH;
+    static constexpr int BW = TMA_BW, BH = TMA_BH;
+    static constexpr int UROWS = TH + 2 * R, UCH = TileGeom<R>::CH, LDC = UCH;   // warps read one row: no pad
     static constexpr int al(int x) { return (x + 127) & ~127; }
     static constexpr int S_P = al(PW * PH * 4), S_B = al(BW * BH * 4), S_G = al(TW * TH * 4);
-    static constexpr int O_P = 0, O_W1 = S_P, O_W2 = 2 * S_P, O_B1 = 3 * S_P, O_B2 = O_B1 + S_B;
-    static constexpr int O_G = O_B2 + S_B, O_U = O_G + S_G, O_BAR = O_U + LDC * UROWS * 16;
+    static constexpr int S_U = al(LDC * UROWS * 16), S_BG = 2 * S_B + S_G;
+    static constexpr int O_P = 0, O_W1 = S_P, O_W2 = 2 * S_P, O_U = 3 * S_P;
+    static constexpr int O_B1 = O_U, O_B2 = O_U + S_B, O_G = O_U + 2 * S_B;   // group 2 reuses the u region
+    static constexpr int O_BAR = O_U + (S_U > S_BG ? S_U : S_BG);
     static constexpr int BYTES = O_BAR + 16 + 128;       // + alignment slack of the dynamic base
-    static constexpr uint32_t TX = (uint32_t)(3 * PW * PH + 2 * BW * BH + TW * TH) * 4;
+    static constexpr uint32_t TX1 = (uint32_t)(3 * PW * PH) * 4, TX2 = (uint32_t)(2 * BW * BH + TW * TH) * 4;
 };
 
 template <int R, int SHAPE, bool LEQ>
-__global__ void __launch_bounds__(256, 2) k_rhs_tma(const __grid_constant__ RhsMaps maps,
+__global__ void __launch_bounds__(256, 3) k_rhs_tma(const __grid_constant__ RhsMaps maps,
                                                     const float* __restrict__ phi, float* __restrict__ D,
                                                     StencilArgs a) {
     using G = TmaGeom<R>;
@@ -647,19 +653,19 @@ __global__ void __launch_bounds__(256, 2) k_rhs_tma(const __grid_constant__ RhsM
     uint64_t* bar = reinterpret_cast<uint64_t*>(sm + G::O_BAR);
     const int img = blockIdx.z, row0 = blockIdx.y * G::TH, col0 = blockIdx.x * G::TW;
     const int tid = threadIdx.y * 32 + threadIdx.x;
-    if (tid == 0) mbar_init(bar, 1);
+    const int ar = a.gh + row0;   // allocation row of local row row0
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+    }
     __syncthreads();
     if (tid == 0) {
-        mbar_expect_tx(bar, G::TX);
-        const int ar = a.gh + row0;   // allocation row of local row row0
-        tma_load_3d(Ps, &maps.phi, bar, col0 - G::CA, ar - G::HR, img);
-        tma_load_3d(W1s, &maps.w, bar, col0 - G::CA, ar - G::HR, 2 * img);
-        tma_load_3d(W2s, &maps.w, bar, col0 - G::CA, ar - G::HR, 2 * img + 1);
-        tma_load_3d(B1s, &maps.b, bar, col0 - 4, ar - 1, 2 * img);
-        tma_load_3d(B2s, &maps.b, bar, col0 - 4, ar - 1, 2 * img + 1);
-        tma_load_3d(Gs, &maps.g, bar, col0, ar, img);
+        mbar_expect_tx(&bar[0], G::TX1);
+        tma_load_3d(Ps, &maps.phi, &bar[0], col0 - G::CA, ar - G::HR, img);
+        tma_load_3d(W1s, &maps.w, &bar[0], col0 - G::CA, ar - G::HR, 2 * img);
+        tma_load_3d(W2s, &maps.w, &bar[0], col0 - G::CA, ar - G::HR, 2 * img + 1);
     }
-    mbar_wait(bar, 0);
+    mbar_wait(&bar[0], 0);
     // u = h(phi) w over the tile + R halo, as 16-byte chunks (2 px x 2 channels) in TileGeom's layout
     for (int k = tid; k < G::UROWS * G::UCH; k += 256) {
         const int r = k / G::UCH, f = k - r * G::UCH;
@@ -678,9 +684,19 @@ __global__ void __launch_bounds__(256, 2) k_rhs_tma(const __grid_constant__ RhsM
     __syncthreads();
     const int r0 = threadIdx.y * G::RT, c0 = threadIdx.x * ST_CT;
     const int M = a.M, N = a.N, gj = col0 + c0;
-    if (gj >= N || row0 + r0 >= M) return;
+    const bool active = gj < N && row0 + r0 < M;
     float2 v[G::RT][ST_CT];
-    window_block<R, SHAPE, G::RT>(U, r0, c0, a.e, v);
+    if (active) window_block<R, SHAPE, G::RT, G::LDC>(U, r0, c0, a.e, v);
+    __syncthreads();   // u is dead: group 2 lands in its place
+    if (tid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads of u before async writes
+        mbar_expect_tx(&bar[1], G::TX2);
+        tma_load_3d(B1s, &maps.b, &bar[1], col0 - 4, ar - 1, 2 * img);
+        tma_load_3d(B2s, &maps.b, &bar[1], col0 - 4, ar - 1, 2 * img + 1);
+        tma_load_3d(Gs, &maps.g, &bar[1], col0, ar, img);
+    }
+    if (!active) return;
+    mbar_wait(&bar[1], 0);
     constexpr int CT = ST_CT;
     const float* ph = phi + img * a.plane;
     float* Do = D + img * a.plane;

@@ -301,7 +301,7 @@ sr_status configure(sr_sb_ctx* c) {
                 RhsMaps& m = c->tmaps[u];
                 mok = mok && encode_map3d(&m.phi, c->phi_base, N, rows, B, pw, ph) &&
                       encode_map3d(&m.w, c->w_base[u], N, rows, 2 * B, pw, ph) &&
-                      encode_map3d(&m.b, c->b_base, N, rows, 2 * B, ST_TW + 8, TMA_TH + 1) &&
+                      encode_map3d(&m.b, c->b_base, N, rows, 2 * B, TMA_BW, TMA_BH) &&
                       encode_map3d(&m.g, c->g_base, N, rows, B, ST_TW, TMA_TH);
             }
             if (!mok) return fail(c, SR_ERR_CUDA, "cuTensorMapEncodeTiled failed");

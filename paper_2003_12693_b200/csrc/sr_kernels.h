@@ -11,6 +11,7 @@ typedef void (*RowInvKernel)(const float2*, float*, const float2*, const float2*
 typedef void (*ColKernel)(float2*, const float2*, const float*, const float*, FftColArgs);
 typedef void (*RhsKernel)(const float*, const float*, const float*, const float*, float*, StencilArgs);
 typedef void (*RhsTmaKernel)(const RhsMaps, const float*, float*, StencilArgs);
+typedef void (*WbTmaKernel)(const RhsMaps, float*, float*, int*, StencilArgs);
 typedef void (*WbKernel)(const float*, const float*, float*, float*, const float*, int*, StencilArgs);
 
 RowKernel pick_row_fwd(int log2_h);       // fft_r2c.cu
@@ -19,10 +20,11 @@ ColKernel pick_col(int log2_m);           // fft_cols.cu
 // stencil_r<R>.cu; returns false if R is unsupported.  smem = dynamic shared bytes.
 bool pick_stencil(int R, int shape, bool leq, RhsKernel& rhs, WbKernel (&wb)[2][2], WbKernel& wb_mon, int& smem);
 
-bool pick_rhs_tma(int R, int shape, bool leq, RhsTmaKernel& k, int& smem);
+bool pick_tma(int R, int shape, bool leq, RhsTmaKernel& k, WbTmaKernel (&wb)[2][2], WbTmaKernel& wb_mon,
+              int& smem_rhs, int& smem_wb);
 
 #define SRSB_DECLARE_STENCIL(R) bool pick_stencil_r##R(int shape, bool leq, RhsKernel& rhs, WbKernel (&wb)[2][2], WbKernel& wb_mon, int& smem); \
-    bool pick_rhs_tma_r##R(int shape, bool leq, RhsTmaKernel& k, int& smem);
+    bool pick_tma_r##R(int shape, bool leq, RhsTmaKernel& k, WbTmaKernel (&wb)[2][2], WbTmaKernel& wb_mon, int& smem_rhs, int& smem_wb);
 SRSB_DECLARE_STENCIL(0) SRSB_DECLARE_STENCIL(1) SRSB_DECLARE_STENCIL(2) SRSB_DECLARE_STENCIL(3)
 SRSB_DECLARE_STENCIL(4) SRSB_DECLARE_STENCIL(5) SRSB_DECLARE_STENCIL(6) SRSB_DECLARE_STENCIL(7)
 SRSB_DECLARE_STENCIL(8)

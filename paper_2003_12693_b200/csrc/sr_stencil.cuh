@@ -467,6 +467,55 @@ __device__ __forceinline__ void project_w(int mode, float& x, float& y) {
     }
 }
 
+// One pixel of the w/b update.  ps, pn, pr: phi at (i, j), (i+1, j), (i, j+1); has_dn / has_rt: the
+// forward differences exist (not the last global row / column, Eq. 35).  wa, wb2: w^k at the pixel
+// (monitor only).  Outputs w^{k+1} = (x, y) and b^{k+1} = (nb1, nb2).
+template <int MODE, bool UPDATE_B, bool LEQ, bool MON>
+__device__ __forceinline__ void wb_pixel(const StencilArgs& a, float ps, float pn, float pr, bool has_dn, bool has_rt,
+                                         float b1, float b2, float g, float2 v, float wa, float wb2, float& x,
+                                         float& y, float& nb1, float& nb2, bool& bad, float& e_g, float& e_a,
+                                         float& e_r, float& e_pen) {
+    const float gp1 = has_dn ? pn - ps : 0.f;
+    const float gp2 = has_rt ? pr - ps : 0.f;
+    float hh, dd;
+    reg_hd<LEQ>(ps, a.reg, hh, dd);
+    if (MON) {   // energy of Eq. (22) at (phi^{k+1}, w^k, b^k), the state entering the update
+        const float aa = ps * a.reg.inv_eps;
+        const float H = aa > 1.f ? 1.f : (aa < -1.f ? 0.f : 0.5f * (1.f + aa + sinpif(aa) * (1.f / kPi)));
+        e_g += g * sqrtf(wa * wa + wb2 * wb2) * dd;
+        e_a += g * (1.f - H);
+        e_r -= hh * (wa * v.x + wb2 * v.y);
+        const float r1 = wa - gp1 - b1, r2 = wb2 - gp2 - b2;
+        e_pen += 0.5f * a.mu * (r1 * r1 + r2 * r2);
+    }
+    if (MODE == 0) {
+        const float Bx = gp1 + b1 + a.beta2_mu * hh * v.x;
+        const float By = gp2 + b2 + a.beta2_mu * hh * v.y;
+        const float t = a.gamma_mu * g * dd;
+        const float nb2v = Bx * Bx + By * By;
+        if (nb2v > 0.f) {
+            const float inv = rsqrtf(nb2v);              // 1/|B|
+            const float m = fmaxf(1.f - t * inv, 0.f);   // max(|B| - t, 0)/|B|
+            x = m * Bx;
+            y = m * By;
+        } else {
+            x = 0.f;
+            y = 0.f;
+        }
+    } else {
+        const float den = a.gamma * g * dd + a.mu;
+        x = (a.mu * gp1 + a.mu * b1 + 2.f * a.beta * hh * v.x) / den;
+        y = (a.mu * gp2 + a.mu * b2 + 2.f * a.beta * hh * v.y) / den;
+    }
+    project_w(a.w_proj, x, y);
+    nb1 = b1 + gp1 - x;
+    nb2 = b2 + gp2 - y;
+    if (UPDATE_B) {
+        bad |= !(fabsf(nb1) <= a.b_max && fabsf(nb2) <= a.b_max) && a.b_max > 0.f;
+        bad |= !isfinite(nb1) || !isfinite(nb2);
+    }
+}
+
 // MODE 0: threshold (Eq. 41-42); MODE 1: fixed-point sweep (Eq. 38-39).  UPDATE_B: last pass,
 // b += grad phi - w_new (Eq. 23) and the non-finite guard.  w_in is read for v (the halo) only in
 // mode 1 beyond the pixel; in mode 0 w_in = w^k.  b is updated in place (pixel-local).
@@ -523,49 +572,14 @@ __device__ __forceinline__ void wb_tile(float4* __restrict__ U, const float* __r
 #pragma unroll
         for (int c = 0; c < CT; c++) {
             const int j = gj + c;
-            const float ps = p_[c];
-            const float gp1 = (gig < a.Mg - 1) ? pn_[c] - ps : 0.f;
-            const float gp2 = (j < N - 1) ? p_[c + 1] - ps : 0.f;
-            float x, y, hh, dd;
-            reg_hd<LEQ>(ps, a.reg, hh, dd);
-            if (MON) {   // energy of Eq. (22) at (phi^{k+1}, w^k, b^k), the state entering the update
-                const float wa = __ldg(w1 + o + c), wb2 = __ldg(w2 + o + c);
-                const float aa = ps * a.reg.inv_eps;
-                const float H = aa > 1.f ? 1.f : (aa < -1.f ? 0.f : 0.5f * (1.f + aa + sinpif(aa) * (1.f / kPi)));
-                e_g += g_[c] * sqrtf(wa * wa + wb2 * wb2) * dd;
-                e_a += g_[c] * (1.f - H);
-                e_r -= hh * (wa * v[i][c].x + wb2 * v[i][c].y);
-                const float r1 = wa - gp1 - b1_[c], r2 = wb2 - gp2 - b2_[c];
-                e_pen += 0.5f * a.mu * (r1 * r1 + r2 * r2);
+            float wa = 0.f, wb2 = 0.f;
+            if (MON) {
+                wa = __ldg(w1 + o + c);
+                wb2 = __ldg(w2 + o + c);
             }
-            if (MODE == 0) {
-                const float Bx = gp1 + b1_[c] + a.beta2_mu * hh * v[i][c].x;
-                const float By = gp2 + b2_[c] + a.beta2_mu * hh * v[i][c].y;
-                const float t = a.gamma_mu * g_[c] * dd;
-                const float nb2v = Bx * Bx + By * By;
-                if (nb2v > 0.f) {
-                    const float inv = rsqrtf(nb2v);              // 1/|B|
-                    const float m = fmaxf(1.f - t * inv, 0.f);   // max(|B| - t, 0)/|B|
-                    x = m * Bx;
-                    y = m * By;
-                } else {
-                    x = 0.f;
-                    y = 0.f;
-                }
-            } else {
-                const float den = a.gamma * g_[c] * dd + a.mu;
-                x = (a.mu * gp1 + a.mu * b1_[c] + 2.f * a.beta * hh * v[i][c].x) / den;
-                y = (a.mu * gp2 + a.mu * b2_[c] + 2.f * a.beta * hh * v[i][c].y) / den;
-            }
-            project_w(a.w_proj, x, y);
-            n1[c] = x;
-            n2[c] = y;
-            nb1[c] = b1_[c] + gp1 - x;
-            nb2[c] = b2_[c] + gp2 - y;
-            if (UPDATE_B) {
-                bad |= !(fabsf(nb1[c]) <= a.b_max && fabsf(nb2[c]) <= a.b_max) && a.b_max > 0.f;
-                bad |= !isfinite(nb1[c]) || !isfinite(nb2[c]);
-            }
+            wb_pixel<MODE, UPDATE_B, LEQ, MON>(a, p_[c], pn_[c], p_[c + 1], gig < a.Mg - 1, j < N - 1, b1_[c], b2_[c],
+                                               g_[c], v[i][c], wa, wb2, n1[c], n2[c], nb1[c], nb2[c], bad, e_g, e_a,
+                                               e_r, e_pen);
         }
         stv<CT>(o1 + o, n1);
         stv<CT>(o2 + o, n2);
@@ -607,6 +621,7 @@ __global__ void __launch_bounds__(32 * ST_BY, ST_MINB) k_rhs(const float* __rest
 // outside are zero-filled by the TMA unit (w = 0 -> u = 0, reading Q5).
 struct RhsMaps {
     CUtensorMap phi, w, b, g;   // phi / w: box PW x PH; b: BW x BH; g: TW x TH (TmaGeom)
+    CUtensorMap bt;             // b, box TW x TH (the w/b update reads b at the tile only)
 };
 
 constexpr int TMA_TH = 32;                                            // tile rows of the TMA kernels
@@ -750,6 +765,133 @@ __global__ void __launch_bounds__(256, 3) k_rhs_tma(const __grid_constant__ RhsM
             out[c] = a.aos ? ps + a.tau * t : a.tau * (t + a.mu * lap);
         }
         stv<CT>(Do + (long long)gi * N + gj, out);
+    }
+}
+
+// ------------------------------------------------------------------ TMA-staged w/b update (k_wb_tma)
+// Data movement of k_rhs_tma for the w/b update: group 1 = phi, w^k (tile + window halo; the box's
+// row / column halo also holds the forward neighbours of Eq. 35), group 2 = b1, b2, g at the tile,
+// landing in the dead u region after the window sums.  The per-pixel arithmetic is wb_pixel, shared
+// with wb_tile.  b is updated in place (pixel-local), w^{k+1} goes to the other ping-pong buffer.
+template <int R>
+struct WbGeom {
+    using T = TmaGeom<R>;
+    static constexpr int TH = T::TH, TW = T::TW, RT = T::RT, HR = T::HR, CA = T::CA, PW = T::PW, PH = T::PH;
+    static constexpr int UROWS = T::UROWS, UCH = T::UCH, LDC = T::LDC, RA = T::RA;
+    static constexpr int S_T = T::al(TW * TH * 4);       // one tile-sized field (b1, b2, g)
+    static constexpr int O_P = 0, O_W1 = T::S_P, O_W2 = 2 * T::S_P, O_U = 3 * T::S_P;
+    static constexpr int O_B1 = O_U, O_B2 = O_U + S_T, O_G = O_U + 2 * S_T;
+    static constexpr int O_BAR = O_U + (T::S_U > 3 * S_T ? T::S_U : 3 * S_T);
+    static constexpr int BYTES = O_BAR + 16 + 128;
+    static constexpr uint32_t TX1 = T::TX1, TX2 = (uint32_t)(3 * TW * TH) * 4;
+};
+
+template <int R, int SHAPE, int MODE, bool UPDATE_B, bool LEQ, bool MON = false>
+__global__ void __launch_bounds__(256, 3) k_wb_tma(const __grid_constant__ RhsMaps maps, float* __restrict__ w_out,
+                                                   float* __restrict__ bv, int* __restrict__ flag, StencilArgs a) {
+    using G = WbGeom<R>;
+    extern __shared__ unsigned char sm_raw[];
+    unsigned char* sm = sm_raw + ((128 - (smem_u32(sm_raw) & 127)) & 127);
+    float* Ps = reinterpret_cast<float*>(sm + G::O_P);
+    float* W1s = reinterpret_cast<float*>(sm + G::O_W1);
+    float* W2s = reinterpret_cast<float*>(sm + G::O_W2);
+    float* B1s = reinterpret_cast<float*>(sm + G::O_B1);
+    float* B2s = reinterpret_cast<float*>(sm + G::O_B2);
+    float* Gs = reinterpret_cast<float*>(sm + G::O_G);
+    float4* U = reinterpret_cast<float4*>(sm + G::O_U);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + G::O_BAR);
+    const int img = blockIdx.z, row0 = blockIdx.y * G::TH, col0 = blockIdx.x * G::TW;
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    const int ar = a.gh + row0;
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        mbar_expect_tx(&bar[0], G::TX1);
+        tma_load_3d(Ps, &maps.phi, &bar[0], col0 - G::CA, ar - G::HR, img);
+        tma_load_3d(W1s, &maps.w, &bar[0], col0 - G::CA, ar - G::HR, 2 * img);
+        tma_load_3d(W2s, &maps.w, &bar[0], col0 - G::CA, ar - G::HR, 2 * img + 1);
+    }
+    mbar_wait(&bar[0], 0);
+    for (int k = tid; k < G::UROWS * G::UCH; k += 256) {
+        const int r = k / G::UCH, f = k - r * G::UCH;
+        const int gi = row0 - R + r;
+        float4 A = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (gi + a.row_off >= 0 && gi + a.row_off < a.Mg) {
+            const int o = (r + G::HR - R) * G::PW + (G::CA - G::RA) + 2 * f;
+            const float2 P = *reinterpret_cast<const float2*>(Ps + o);
+            const float2 X = *reinterpret_cast<const float2*>(W1s + o);
+            const float2 Y = *reinterpret_cast<const float2*>(W2s + o);
+            const float h0 = reg_h<LEQ>(P.x, a.reg), h1 = reg_h<LEQ>(P.y, a.reg);
+            A = make_float4(h0 * X.x, h0 * Y.x, h1 * X.y, h1 * Y.y);
+        }
+        U[r * G::LDC + swz(f)] = A;
+    }
+    __syncthreads();
+    const int r0 = threadIdx.y * G::RT, c0 = threadIdx.x * ST_CT;
+    const int M = a.M, N = a.N, gj = col0 + c0;
+    const bool active = gj < N && row0 + r0 < M;
+    float2 v[G::RT][ST_CT];
+    if (active) window_block<R, SHAPE, G::RT, G::LDC>(U, r0, c0, a.e, v);
+    __syncthreads();   // u is dead: group 2 lands in its place
+    if (tid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(&bar[1], G::TX2);
+        tma_load_3d(B1s, &maps.bt, &bar[1], col0, ar, 2 * img);
+        tma_load_3d(B2s, &maps.bt, &bar[1], col0, ar, 2 * img + 1);
+        tma_load_3d(Gs, &maps.g, &bar[1], col0, ar, img);
+    }
+    if (!active) return;
+    mbar_wait(&bar[1], 0);
+    constexpr int CT = ST_CT;
+    bool bad = false;
+    float e_g = 0.f, e_a = 0.f, e_r = 0.f, e_pen = 0.f;
+    float* o1 = w_out + img * 2 * a.plane;
+    float* o2 = o1 + a.plane;
+    float* b1g = bv + img * 2 * a.plane;
+    float* b2g = b1g + a.plane;
+#pragma unroll
+    for (int i = 0; i < G::RT; i++) {
+        const int tr = r0 + i, gi = row0 + tr;
+        if (gi >= M) break;
+        const int gig = gi + a.row_off;
+        const float* prow = Ps + (G::HR + tr) * G::PW + G::CA + c0;
+        const float2 P = *reinterpret_cast<const float2*>(prow);
+        const float2 Pn = *reinterpret_cast<const float2*>(prow + G::PW);
+        const float p_[CT + 1] = {P.x, P.y, prow[CT]}, pn_[CT] = {Pn.x, Pn.y};
+        const float2 B1 = *reinterpret_cast<const float2*>(B1s + tr * G::TW + c0);
+        const float2 B2 = *reinterpret_cast<const float2*>(B2s + tr * G::TW + c0);
+        const float2 Gv = *reinterpret_cast<const float2*>(Gs + tr * G::TW + c0);
+        const float b1_[CT] = {B1.x, B1.y}, b2_[CT] = {B2.x, B2.y}, g_[CT] = {Gv.x, Gv.y};
+        float wa_[CT] = {0.f, 0.f}, wb_[CT] = {0.f, 0.f};
+        if (MON) {
+            const float2 W1 = *reinterpret_cast<const float2*>(W1s + (G::HR + tr) * G::PW + G::CA + c0);
+            const float2 W2 = *reinterpret_cast<const float2*>(W2s + (G::HR + tr) * G::PW + G::CA + c0);
+            wa_[0] = W1.x; wa_[1] = W1.y; wb_[0] = W2.x; wb_[1] = W2.y;
+        }
+        float n1[CT], n2[CT], nb1[CT], nb2[CT];
+#pragma unroll
+        for (int c = 0; c < CT; c++)
+            wb_pixel<MODE, UPDATE_B, LEQ, MON>(a, p_[c], pn_[c], p_[c + 1], gig < a.Mg - 1, gj + c < N - 1, b1_[c],
+                                               b2_[c], g_[c], v[i][c], wa_[c], wb_[c], n1[c], n2[c], nb1[c], nb2[c],
+                                               bad, e_g, e_a, e_r, e_pen);
+        const long long o = (long long)gi * N + gj;
+        stv<CT>(o1 + o, n1);
+        stv<CT>(o2 + o, n2);
+        if (UPDATE_B) {
+            stv<CT>(b1g + o, nb1);
+            stv<CT>(b2g + o, nb2);
+        }
+    }
+    if (UPDATE_B && bad) atomicOr(flag, 1);
+    if (MON) {
+        double* st = a.stats + (long long)img * a.stats_stride;
+        warp_accumulate(st + 0, e_g);
+        warp_accumulate(st + 1, e_a);
+        warp_accumulate(st + 2, e_r);
+        warp_accumulate(st + 3, e_pen);
     }
 }
 

@@ -77,10 +77,12 @@ struct sr_sb_ctx {
     RowInvKernel rinv = nullptr;
     ColKernel cols = nullptr;
     RhsKernel rhs = nullptr;
-    RhsTmaKernel rhs_tma = nullptr;   // TMA-staged RHS (default; SRSB_TMA=0 selects k_rhs)
+    RhsTmaKernel rhs_tma = nullptr;   // TMA-staged stencils (default; SRSB_TMA=0 selects k_rhs / k_wb)
+    WbTmaKernel wb_tma[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+    WbTmaKernel wb_tma_mon = nullptr;
     RhsMaps tmaps[2];                 // tensor maps, per w ping-pong buffer
     dim3 tgrid;
-    int tsmem = 0;
+    int tsmem = 0, tsmem_wb = 0;
     WbKernel wb[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
     WbKernel wb_mon = nullptr;     // monitor variant (threshold mode, last pass)
     FftRowArgs ra{};
@@ -293,7 +295,8 @@ sr_status configure(sr_sb_ctx* c) {
     a.gh = c->gh;
     {   // TMA-staged RHS
         const char* e = getenv("SRSB_TMA");
-        if (!(e && e[0] == '0') && pick_rhs_tma(p.window, p.window_shape, p.l == p.epsilon, c->rhs_tma, c->tsmem)) {
+        if (!(e && e[0] == '0') && pick_tma(p.window, p.window_shape, p.l == p.epsilon, c->rhs_tma, c->wb_tma,
+                                             c->wb_tma_mon, c->tsmem, c->tsmem_wb)) {
             const int R = p.window, rows = Ml + 2 * c->gh;
             const int pw = tma_pw(R), ph = tma_ph(R);
             bool mok = true;
@@ -302,11 +305,18 @@ sr_status configure(sr_sb_ctx* c) {
                 mok = mok && encode_map3d(&m.phi, c->phi_base, N, rows, B, pw, ph) &&
                       encode_map3d(&m.w, c->w_base[u], N, rows, 2 * B, pw, ph) &&
                       encode_map3d(&m.b, c->b_base, N, rows, 2 * B, TMA_BW, TMA_BH) &&
-                      encode_map3d(&m.g, c->g_base, N, rows, B, ST_TW, TMA_TH);
+                      encode_map3d(&m.g, c->g_base, N, rows, B, ST_TW, TMA_TH) &&
+                      encode_map3d(&m.bt, c->b_base, N, rows, 2 * B, ST_TW, TMA_TH);
             }
             if (!mok) return fail(c, SR_ERR_CUDA, "cuTensorMapEncodeTiled failed");
             c->tgrid = dim3(a.tiles_x, (Ml + TMA_TH - 1) / TMA_TH, B);
             CK(cudaFuncSetAttribute((const void*)c->rhs_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, c->tsmem));
+            for (int m = 0; m < 2; m++)
+                for (int u = 0; u < 2; u++)
+                    CK(cudaFuncSetAttribute((const void*)c->wb_tma[m][u], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            c->tsmem_wb));
+            CK(cudaFuncSetAttribute((const void*)c->wb_tma_mon, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    c->tsmem_wb));
         } else {
             c->rhs_tma = nullptr;
         }
@@ -418,8 +428,15 @@ void enq_rhs(sr_sb_ctx* c, float* F) {
 }
 void enq_wb_pass(sr_sb_ctx* c, int last) {
     prof_begin(c);
-    WbKernel k = (c->stats && last && c->p.w_mode == SR_W_THRESHOLD) ? c->wb_mon : c->wb[c->p.w_mode][last];
-    k<<<c->sgrid, c->sblock, c->ssmem, c->s>>>(c->phi, c->w[c->wcur], c->w[c->wcur ^ 1], c->b, c->g, c->flag, c->sa);
+    const bool mon = c->stats && last && c->p.w_mode == SR_W_THRESHOLD;
+    if (c->rhs_tma) {
+        WbTmaKernel k = mon ? c->wb_tma_mon : c->wb_tma[c->p.w_mode][last];
+        k<<<c->tgrid, c->sblock, c->tsmem_wb, c->s>>>(c->tmaps[c->wcur], c->w[c->wcur ^ 1], c->b, c->flag, c->sa);
+    } else {
+        WbKernel k = mon ? c->wb_mon : c->wb[c->p.w_mode][last];
+        k<<<c->sgrid, c->sblock, c->ssmem, c->s>>>(c->phi, c->w[c->wcur], c->w[c->wcur ^ 1], c->b, c->g, c->flag,
+                                                   c->sa);
+    }
     prof_end(c, SR_K_WB);
     c->wcur ^= 1;
 }

@@ -15,17 +15,18 @@ bool pick_stencil(int R, int shape, bool leq, RhsKernel& rhs, WbKernel (&wb)[2][
     }
     return false;
 }
-bool pick_rhs_tma(int R, int shape, bool leq, RhsTmaKernel& k, int& smem) {
+bool pick_tma(int R, int shape, bool leq, RhsTmaKernel& k, WbTmaKernel (&wb)[2][2], WbTmaKernel& wb_mon,
+              int& smem_rhs, int& smem_wb) {
     switch (R) {
-        case 0: return pick_rhs_tma_r0(shape, leq, k, smem);
-        case 1: return pick_rhs_tma_r1(shape, leq, k, smem);
-        case 2: return pick_rhs_tma_r2(shape, leq, k, smem);
-        case 3: return pick_rhs_tma_r3(shape, leq, k, smem);
-        case 4: return pick_rhs_tma_r4(shape, leq, k, smem);
-        case 5: return pick_rhs_tma_r5(shape, leq, k, smem);
-        case 6: return pick_rhs_tma_r6(shape, leq, k, smem);
-        case 7: return pick_rhs_tma_r7(shape, leq, k, smem);
-        case 8: return pick_rhs_tma_r8(shape, leq, k, smem);
+        case 0: return pick_tma_r0(shape, leq, k, wb, wb_mon, smem_rhs, smem_wb);
+        case 1: return pick_tma_r1(shape, leq, k, wb, wb_mon, smem_rhs, smem_wb);
+        case 2: return pick_tma_r2(shape, leq, k, wb, wb_mon, smem_rhs, smem_wb);
+        case 3: return pick_tma_r3(shape, leq, k, wb, wb_mon, smem_rhs, smem_wb);
+        case 4: return pick_tma_r4(shape, leq, k, wb, wb_mon, smem_rhs, smem_wb);
+        case 5: return pick_tma_r5(shape, leq, k, wb, wb_mon, smem_rhs, smem_wb);
+        case 6: return pick_tma_r6(shape, leq, k, wb, wb_mon, smem_rhs, smem_wb);
+        case 7: return pick_tma_r7(shape, leq, k, wb, wb_mon, smem_rhs, smem_wb);
+        case 8: return pick_tma_r8(shape, leq, k, wb, wb_mon, smem_rhs, smem_wb);
     }
     return false;
 }

@@ -40,6 +40,12 @@ __device__ __forceinline__ float2 mul2(float2 a, float2 b) {
     asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
     return u2f(d);
 }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
+    unsigned long long d;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
+    return u2f(d);
+}
+__device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
 
 // ------------------------------------------------------------------ regularizers (Eq. 5, 6, 11, 28, 29)
 // All of H(x +- l), delta(x +- l), delta(x), delta'(x) from ONE sincospif(x / eps): the arguments
@@ -152,6 +158,48 @@ __device__ __forceinline__ void reg_hd(float x, const Reg& r, float& h, float& d
     const float sm = s * r.cl - c * r.sl;
     h = H_of(x + r.l, sp, r) * (1.f - H_of(x - r.l, sm, r));
     d = fabsf(x) <= r.eps ? (1.f + c) * (0.5f * r.inv_eps) : 0.f;
+}
+
+// Two adjacent pixels at once (f32x2 arithmetic around the per-lane sincospif), branch-free.
+// h(x) for the u staging:
+template <bool LEQ>
+__device__ __forceinline__ float2 reg_h2(float2 x, const Reg& r) {
+    if constexpr (LEQ) {
+        const float2 a = mul2(x, f2(r.inv_eps));
+        const float2 aa = make_float2(fabsf(a.x), fabsf(a.y));
+        if (aa.x >= 2.f && aa.y >= 2.f) return f2(0.f);   // outside the band (most pixels: skip the sines)
+        const float2 sv = make_float2(sinpif(aa.x), sinpif(aa.y));
+        const float2 h = mul2(fma2(sv, f2(1.f / kPi), sub2(f2(2.f), aa)), f2(0.5f));
+        return make_float2(aa.x >= 2.f ? 0.f : h.x, aa.y >= 2.f ? 0.f : h.y);
+    }
+    return make_float2(reg_h<false>(x.x, r), reg_h<false>(x.y, r));
+}
+// h'(x), delta(x), delta'(x) for the RHS:
+template <bool LEQ>
+__device__ __forceinline__ void reg_rhs2(float2 x, const Reg& r, float2& hp, float2& d, float2& dp) {
+    if constexpr (LEQ) {
+        const float2 a = mul2(x, f2(r.inv_eps));
+        if (fabsf(a.x) >= 2.f && fabsf(a.y) >= 2.f) {   // outside the band: all three vanish
+            hp = d = dp = f2(0.f);
+            return;
+        }
+        float2 sv, cv;
+        sincospif(a.x, &sv.x, &cv.x);
+        sincospif(a.y, &sv.y, &cv.y);
+        const float k = 0.5f * r.inv_eps;
+        const float2 hpm = mul2(sub2(f2(1.f), cv), f2(k));          // (1 - cospi a) k >= 0
+        const float2 dm = fma2(cv, f2(k), f2(k));                    // (1 + cospi a) k
+        const float2 dpm = mul2(sv, f2(-(0.5f * kPi) * r.inv_eps * r.inv_eps));
+        const float ax = fabsf(a.x), ay = fabsf(a.y);
+        hp = make_float2(ax >= 2.f ? 0.f : copysignf(hpm.x, -a.x), ay >= 2.f ? 0.f : copysignf(hpm.y, -a.y));
+        d = make_float2(ax <= 1.f ? dm.x : 0.f, ay <= 1.f ? dm.y : 0.f);
+        dp = make_float2(ax <= 1.f ? dpm.x : 0.f, ay <= 1.f ? dpm.y : 0.f);
+        return;
+    }
+    const RegVals v0 = reg_all<false>(x.x, r), v1 = reg_all<false>(x.y, r);
+    hp = make_float2(v0.hp, v1.hp);
+    d = make_float2(v0.d, v1.d);
+    dp = make_float2(v0.dp, v1.dp);
 }
 
 __host__ __device__ constexpr int isqrt_c(int v) {
@@ -651,6 +699,87 @@ struct TmaGeom {
     static constexpr uint32_t TX1 = (uint32_t)(3 * PW * PH) * 4, TX2 = (uint32_t)(2 * BW * BH + TW * TH) * 4;
 };
 
+// u = h(phi) w over the tile + R halo from the group-1 boxes, as 16-byte chunks (2 px x 2 channels)
+// in TileGeom's layout; rows outside the image give u = 0 (reading Q5).  Branch-free, f32x2.
+template <int R, bool LEQ, class G>
+__device__ __forceinline__ void stage_u_tma(float4* __restrict__ U, const float* Ps, const float* W1s,
+                                            const float* W2s, int row0, int tid, const StencilArgs& a) {
+    for (int k = tid; k < G::UROWS * G::UCH; k += 256) {
+        const int r = k / G::UCH, f = k - r * G::UCH;
+        const int gr = row0 - R + r + a.row_off;   // global row
+        const int o = (r + G::HR - R) * G::PW + (G::CA - G::RA) + 2 * f;
+        const float2 P = *reinterpret_cast<const float2*>(Ps + o);
+        const float2 X = *reinterpret_cast<const float2*>(W1s + o);
+        const float2 Y = *reinterpret_cast<const float2*>(W2s + o);
+        const float2 h = reg_h2<LEQ>(P, a.reg);
+        const float2 hx = mul2(h, X), hy = mul2(h, Y);
+        const bool in = gr >= 0 && gr < a.Mg;
+        U[r * G::LDC + swz(f)] = in ? make_float4(hx.x, hy.x, hx.y, hy.y) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+}
+
+// The pointwise part of Eq. (37) (increment form) for the thread's RT x 2 block,
+// both pixels of a row in f32x2.  EDGE = false: the tile touches no image boundary (no masks, no
+// periodic wrap loads, no ragged rows).
+template <int R, bool LEQ, bool EDGE, class G>
+__device__ __forceinline__ void rhs_points_tma(const float* Ps, const float* W1s, const float* W2s, const float* B1s,
+                                               const float* B2s, const float* Gs, const float* __restrict__ phi,
+                                               float* __restrict__ D, const float2 (&v)[G::RT][ST_CT], int img,
+                                               int row0, int r0, int c0, int col0, const StencilArgs& a) {
+    const int M = a.M, N = a.N, gj = col0 + c0;
+    const float* ph = phi + img * a.plane;
+    float* Do = D + img * a.plane;
+#pragma unroll
+    for (int i = 0; i < G::RT; i++) {
+        const int tr = r0 + i, gi = row0 + tr;
+        if (EDGE && gi >= M) break;
+        const float* prow = Ps + (G::HR + tr) * G::PW + G::CA + c0;
+        const float* w1r = W1s + (G::HR + tr) * G::PW + G::CA + c0;
+        const float* w2r = W2s + (G::HR + tr) * G::PW + G::CA + c0;
+        const float* b1r = B1s + (1 + tr) * G::BW + 4 + c0;
+        const float* b2r = B2s + (1 + tr) * G::BW + 4 + c0;
+        const float2 P = *reinterpret_cast<const float2*>(prow);
+        float2 Pu = *reinterpret_cast<const float2*>(prow - G::PW);
+        float2 Pd = *reinterpret_cast<const float2*>(prow + G::PW);
+        float pl = prow[-1], pr = prow[ST_CT];
+        const float2 W1 = *reinterpret_cast<const float2*>(w1r), W2 = *reinterpret_cast<const float2*>(w2r);
+        const float2 W1u = *reinterpret_cast<const float2*>(w1r - G::PW);
+        const float2 B1 = *reinterpret_cast<const float2*>(b1r), B2 = *reinterpret_cast<const float2*>(b2r);
+        const float2 B1u = *reinterpret_cast<const float2*>(b1r - G::BW);
+        const float2 Gv = *reinterpret_cast<const float2*>(Gs + tr * G::TW + c0);
+        float2 c1 = sub2(B1, W1), c1u = sub2(B1u, W1u), c2 = sub2(B2, W2);
+        float2 c2l = make_float2(b2r[-1] - w2r[-1], c2.x);   // (b2 - w2) at columns gj - 1, gj
+        if (EDGE) {
+            const int gig = gi + a.row_off;
+            if (!a.slab) {   // periodic rows of Eq. (32) wrap in-kernel for a whole image
+                if (gi == 0) Pu = __ldg(reinterpret_cast<const float2*>(ph + (long long)(M - 1) * N + gj));
+                if (gi == M - 1) Pd = __ldg(reinterpret_cast<const float2*>(ph + gj));
+            }
+            if (gj == 0) pl = __ldg(ph + (long long)gi * N + N - 1);
+            if (gj + ST_CT == N) pr = __ldg(ph + (long long)gi * N);
+            // Eq. (36) / Q6: terms outside the image are dropped (x + 0 and x - 0 are exact)
+            if (gig >= a.Mg - 1) c1 = f2(0.f);
+            if (gig <= 0) c1u = f2(0.f);
+            if (gj + 1 >= N - 1) c2.y = 0.f;
+            if (gj == 0) c2l.x = 0.f;
+        }
+        const float2 lap = add2(add2(sub2(Pu, P), sub2(Pd, P)),
+                                add2(sub2(make_float2(pl, P.x), P), sub2(make_float2(P.y, pr), P)));
+        const float2 dv = sub2(add2(sub2(c1, c1u), c2), c2l);
+        const float2 n2 = fma2(W1, W1, mul2(W2, W2));
+        const float2 wn = make_float2(sqrt_approx(n2.x), sqrt_approx(n2.y));
+        const float2 wv = fma2(W1, make_float2(v[i][0].x, v[i][1].x), mul2(W2, make_float2(v[i][0].y, v[i][1].y)));
+        float2 hp, dd, dp;
+        reg_rhs2<LEQ>(P, a.reg, hp, dd, dp);
+        // t = g (alpha delta - gamma |w| delta') + 2 beta h' w.v + mu div(b - w)
+        float2 t = mul2(Gv, fma2(f2(a.alpha), dd, mul2(f2(-a.gamma), mul2(wn, dp))));
+        t = fma2(f2(2.f * a.beta), mul2(hp, wv), t);
+        t = fma2(f2(a.mu), dv, t);
+        const float2 out = a.aos ? fma2(f2(a.tau), t, P) : mul2(f2(a.tau), fma2(f2(a.mu), lap, t));
+        *reinterpret_cast<float2*>(Do + (long long)gi * N + gj) = out;
+    }
+}
+
 template <int R, int SHAPE, bool LEQ>
 __global__ void __launch_bounds__(256, 3) k_rhs_tma(const __grid_constant__ RhsMaps maps,
                                                     const float* __restrict__ phi, float* __restrict__ D,
@@ -682,20 +811,7 @@ __global__ void __launch_bounds__(256, 3) k_rhs_tma(const __grid_constant__ RhsM
     }
     mbar_wait(&bar[0], 0);
     // u = h(phi) w over the tile + R halo, as 16-byte chunks (2 px x 2 channels) in TileGeom's layout
-    for (int k = tid; k < G::UROWS * G::UCH; k += 256) {
-        const int r = k / G::UCH, f = k - r * G::UCH;
-        const int gi = row0 - R + r;
-        float4 A = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (gi + a.row_off >= 0 && gi + a.row_off < a.Mg) {
-            const int o = (r + G::HR - R) * G::PW + (G::CA - G::RA) + 2 * f;
-            const float2 P = *reinterpret_cast<const float2*>(Ps + o);
-            const float2 X = *reinterpret_cast<const float2*>(W1s + o);
-            const float2 Y = *reinterpret_cast<const float2*>(W2s + o);
-            const float h0 = reg_h<LEQ>(P.x, a.reg), h1 = reg_h<LEQ>(P.y, a.reg);
-            A = make_float4(h0 * X.x, h0 * Y.x, h1 * X.y, h1 * Y.y);
-        }
-        U[r * G::LDC + swz(f)] = A;
-    }
+    stage_u_tma<R, LEQ, G>(U, Ps, W1s, W2s, row0, tid, a);
     __syncthreads();
     const int r0 = threadIdx.y * G::RT, c0 = threadIdx.x * ST_CT;
     const int M = a.M, N = a.N, gj = col0 + c0;
@@ -712,60 +828,13 @@ __global__ void __launch_bounds__(256, 3) k_rhs_tma(const __grid_constant__ RhsM
     }
     if (!active) return;
     mbar_wait(&bar[1], 0);
-    constexpr int CT = ST_CT;
-    const float* ph = phi + img * a.plane;
-    float* Do = D + img * a.plane;
-#pragma unroll
-    for (int i = 0; i < G::RT; i++) {
-        const int tr = r0 + i, gi = row0 + tr;
-        if (gi >= M) break;
-        const int gig = gi + a.row_off;
-        const float* prow = Ps + (G::HR + tr) * G::PW + G::CA + c0;
-        const float* w1r = W1s + (G::HR + tr) * G::PW + G::CA + c0;
-        const float* w2r = W2s + (G::HR + tr) * G::PW + G::CA + c0;
-        const float* b1r = B1s + (1 + tr) * G::BW + 4 + c0;
-        const float* b2r = B2s + (1 + tr) * G::BW + 4 + c0;
-        const float2 P = *reinterpret_cast<const float2*>(prow);
-        float2 Pu = *reinterpret_cast<const float2*>(prow - G::PW);
-        float2 Pd = *reinterpret_cast<const float2*>(prow + G::PW);
-        if (!a.slab) {   // periodic rows of Eq. (32) wrap in-kernel for a whole image
-            if (gi == 0) Pu = __ldg(reinterpret_cast<const float2*>(ph + (long long)(M - 1) * N + gj));
-            if (gi == M - 1) Pd = __ldg(reinterpret_cast<const float2*>(ph + gj));
-        }
-        const float pl = gj == 0 ? __ldg(ph + (long long)gi * N + N - 1) : prow[-1];
-        const float pr = gj + CT == N ? __ldg(ph + (long long)gi * N) : prow[CT];
-        const float2 W1 = *reinterpret_cast<const float2*>(w1r), W2 = *reinterpret_cast<const float2*>(w2r);
-        const float2 W1u = *reinterpret_cast<const float2*>(w1r - G::PW);
-        const float2 B1 = *reinterpret_cast<const float2*>(b1r), B2 = *reinterpret_cast<const float2*>(b2r);
-        const float2 B1u = *reinterpret_cast<const float2*>(b1r - G::BW);
-        const float2 Gv = *reinterpret_cast<const float2*>(Gs + tr * G::TW + c0);
-        const float c2l0 = b2r[-1] - w2r[-1];   // (b2 - w2) at column gj - 1 (unused at gj = 0)
-        const float ps_[CT] = {P.x, P.y}, pu_[CT] = {Pu.x, Pu.y}, pd_[CT] = {Pd.x, Pd.y};
-        const float w1_[CT] = {W1.x, W1.y}, w2_[CT] = {W2.x, W2.y}, g_[CT] = {Gv.x, Gv.y};
-        const float c1_[CT] = {B1.x - W1.x, B1.y - W1.y}, c1u_[CT] = {B1u.x - W1u.x, B1u.y - W1u.y};
-        const float c2_[CT] = {B2.x - W2.x, B2.y - W2.y};
-        float out[CT];
-#pragma unroll
-        for (int c = 0; c < CT; c++) {
-            const int j = gj + c;
-            float dv = 0.f;
-            if (gig < a.Mg - 1) dv += c1_[c];
-            if (gig > 0) dv -= c1u_[c];
-            if (j < N - 1) dv += c2_[c];
-            if (j > 0) dv -= (c == 0 ? c2l0 : c2_[c - 1]);
-            const float ps = ps_[c];
-            const float left = c > 0 ? ps_[c > 0 ? c - 1 : 0] : pl;
-            const float right = c < CT - 1 ? ps_[c < CT - 1 ? c + 1 : 0] : pr;
-            const float lap = ((pu_[c] - ps) + (pd_[c] - ps)) + ((left - ps) + (right - ps));
-            const float wn = sqrt_approx(w1_[c] * w1_[c] + w2_[c] * w2_[c]);
-            const float wv = w1_[c] * v[i][c].x + w2_[c] * v[i][c].y;
-            const RegVals rv = reg_all<LEQ>(ps, a.reg);
-            const float t = -a.gamma * g_[c] * wn * rv.dp + a.alpha * g_[c] * rv.d + 2.f * a.beta * rv.hp * wv +
-                            a.mu * dv;
-            out[c] = a.aos ? ps + a.tau * t : a.tau * (t + a.mu * lap);
-        }
-        stv<CT>(Do + (long long)gi * N + gj, out);
-    }
+    // interior tiles (no image boundary, no ragged rows) take the check-free path
+    const bool edge = row0 + a.row_off == 0 || row0 + G::TH + a.row_off >= a.Mg || row0 + G::TH > M || col0 == 0 ||
+                      col0 + G::TW >= N;
+    if (edge)
+        rhs_points_tma<R, LEQ, true, G>(Ps, W1s, W2s, B1s, B2s, Gs, phi, D, v, img, row0, r0, c0, col0, a);
+    else
+        rhs_points_tma<R, LEQ, false, G>(Ps, W1s, W2s, B1s, B2s, Gs, phi, D, v, img, row0, r0, c0, col0, a);
 }
 
 // ------------------------------------------------------------------ TMA-staged w/b update (k_wb_tma)
@@ -815,20 +884,7 @@ __global__ void __launch_bounds__(256, 3) k_wb_tma(const __grid_constant__ RhsMa
         tma_load_3d(W2s, &maps.w, &bar[0], col0 - G::CA, ar - G::HR, 2 * img + 1);
     }
     mbar_wait(&bar[0], 0);
-    for (int k = tid; k < G::UROWS * G::UCH; k += 256) {
-        const int r = k / G::UCH, f = k - r * G::UCH;
-        const int gi = row0 - R + r;
-        float4 A = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (gi + a.row_off >= 0 && gi + a.row_off < a.Mg) {
-            const int o = (r + G::HR - R) * G::PW + (G::CA - G::RA) + 2 * f;
-            const float2 P = *reinterpret_cast<const float2*>(Ps + o);
-            const float2 X = *reinterpret_cast<const float2*>(W1s + o);
-            const float2 Y = *reinterpret_cast<const float2*>(W2s + o);
-            const float h0 = reg_h<LEQ>(P.x, a.reg), h1 = reg_h<LEQ>(P.y, a.reg);
-            A = make_float4(h0 * X.x, h0 * Y.x, h1 * X.y, h1 * Y.y);
-        }
-        U[r * G::LDC + swz(f)] = A;
-    }
+    stage_u_tma<R, LEQ, G>(U, Ps, W1s, W2s, row0, tid, a);
     __syncthreads();
     const int r0 = threadIdx.y * G::RT, c0 = threadIdx.x * ST_CT;
     const int M = a.M, N = a.N, gj = col0 + c0;

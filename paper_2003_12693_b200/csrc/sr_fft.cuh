@@ -23,6 +23,10 @@
 
 namespace srsb {
 
+#ifndef SRSB_COLS_MAXNREG
+#define SRSB_COLS_MAXNREG 96   // 64-thread column CTAs: 96 registers -> 10 CTAs / SM without spills (128: 8)
+#endif
+
 // float2 shared-memory index with one pad slot per 16 complex values (128 B): strided butterfly
 // accesses with power-of-two strides <= 16 hit 16 distinct 8-byte bank pairs per half-warp.
 __device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
@@ -220,7 +224,7 @@ struct FftColArgs {
 // Column pass: forward FFT, divide by the symbol, inverse FFT, in place.  Threads of one column
 // are consecutive (t fastest), so a warp works inside one transform.
 template <int LOGM, int LOGE>
-__global__ void __launch_bounds__(512) k_cols_solve(float2* __restrict__ spec, const float2* __restrict__ twM,
+__global__ void __maxnreg__(SRSB_COLS_MAXNREG) k_cols_solve(float2* __restrict__ spec, const float2* __restrict__ twM,
                                                        const float* __restrict__ cM, const float* __restrict__ cN,
                                                        FftColArgs a) {
     constexpr int M = 1 << LOGM, E = 1 << LOGE, T = M / E;
@@ -234,16 +238,15 @@ __global__ void __launch_bounds__(512) k_cols_solve(float2* __restrict__ spec, c
     const int kg = k2l >> a.lg_G, cc = k2l & (G - 1);
     float2* base = spec + b * a.bstride + cc;
     float2* sm = smem2 + cl * a.SC;
-    long long addr[E];
-#pragma unroll
-    for (int u = 0; u < E; u++) {
-        const int m = t + u * T;
+    // element m of the column (recomputed at the store: holding E 64-bit addresses across both FFTs
+    // cost 32 registers)
+    auto addr = [&](int m) -> long long {
         const int s = m >> a.lg_seg, mr = m & ((1 << a.lg_seg) - 1);
-        addr[u] = s * a.seg_stride + ((long long)((kg << a.lg_seg) + mr) << a.lg_G);
-    }
+        return s * a.seg_stride + ((long long)((kg << a.lg_seg) + mr) << a.lg_G);
+    };
     float2 v[E];
 #pragma unroll
-    for (int u = 0; u < E; u++) v[u] = base[addr[u]];
+    for (int u = 0; u < E; u++) v[u] = base[addr(t + u * T)];
     fft_stages<LOGM, LOGE, 0, false>(v, sm, t, twM);
     if (blockIdx.x == 0 && a.k2_off == 0) {  // CTA-uniform: slot 0 packs the real columns k2 = 0, N/2
 #pragma unroll
@@ -281,7 +284,7 @@ __global__ void __launch_bounds__(512) k_cols_solve(float2* __restrict__ spec, c
     }
     fft_stages<LOGM, LOGE, 0, true>(v, sm, t, twM);
 #pragma unroll
-    for (int u = 0; u < E; u++) base[addr[u]] = v[u];
+    for (int u = 0; u < E; u++) base[addr(t + u * T)] = v[u];
 }
 
 // Row pass 2: transposed half spectrum -> inverse real FFT -> phi rows (accumulated, clamped).

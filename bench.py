@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--phi-solver", default="fft", choices=["fft", "aos"],
                     help="phi sub-problem: FFT solve Eq. (31)-(33) (north star) or the AOS variant (P:427)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-fft-ref", action="store_true", help="skip the cuFFT reference timing (SURVEY §8(d))")
     ap.add_argument("--no-cpu", action="store_true")
     return ap.parse_args()
 
@@ -149,6 +150,29 @@ def cpu_baseline_oracle(cfg, target_s=12.0):
     return {"value": M * N * k / t / 1e6, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"1 image of {cfg['name']} ({M}x{N}), {k} SB iterations, float64 C oracle, "
                       f"OMP_NUM_THREADS={os.environ.get('OMP_NUM_THREADS')}, {t:.1f} s"}
+
+
+def cufft_reference(nb, M, N, dev, stream, kernels, reps=5):
+    """cuFFT R2C + C2R (torch.fft, i.e. cuFFT) on the same batch of M x N fp32 fields,
+    timed next to our three-pass solve (k_rows_r2c + k_cols_solve + k_rows_c2r, which also applies
+    the symbol and the increment).  Never on the hot path; measured after the timed regions."""
+    import torch
+    x = torch.randn(nb, M, N, device=dev, dtype=torch.float32)
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            y = torch.fft.irfft2(torch.fft.rfft2(x), s=(M, N))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            y = torch.fft.irfft2(torch.fft.rfft2(x), s=(M, N))
+        e1.record(stream)
+        torch.cuda.synchronize()
+    cufft_ms = e0.elapsed_time(e1) / reps
+    ours = sum(kernels[k]["ms_per_launch"] for k in ("rows_r2c", "cols_solve", "rows_c2r") if k in kernels)
+    del x, y
+    return {"cufft_rfft2_irfft2_ms": cufft_ms, "ours_r2c_cols_c2r_ms": ours if ours else None,
+            "batch": nb, "M": M, "N": N,
+            "note": "ours includes the symbol division and the increment/clamp epilogue; cuFFT is transforms only"}
 
 
 def run_reference(args, cfg, rank):
@@ -322,7 +346,8 @@ def main():
                        "share": v[0] / sum(x[0] for x in prof.values()),
                        "GBs": BYTES_PER_PX[k] * px_rank / (v[0] / v[1] / 1e3) / 1e9} for k, v in prof.items()}
         roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                    "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                    "frac": achieved / peak, "frac_vs_datasheet_8TBs": achieved / 8000.0,
+                    "traffic": traffic, "peak_source": peak_src,
                     "bytes_per_px_per_launch": BYTES_PER_PX[dom], "step_model": step_model,
                     "kernels": kernels, "profiled_iteration_ms": iter_ms}
     else:   # slab mode: no per-kernel profile entry; the whole-step model per rank
@@ -361,6 +386,9 @@ def main():
                "d2h_bytes_per_step": int(out_h.numel() * 4) * world, "ms_per_step": ems / args.steps}
 
     launches = args.steps * (4 + K * sv.launches_per_iteration)
+    fft_ref = None
+    if rank == 0 and mode != "slab" and not args.no_fft_ref and "kernels" in roofline:
+        fft_ref = cufft_reference(nb, M, N, dev, stream, roofline["kernels"])
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline_oracle(cfg)
@@ -369,8 +397,9 @@ def main():
                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
                "scaling": "weak" if mode == "replica" else "strong",
                "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": dict(config_json(cfg, world), mode=mode),
+               "value_per_gpu": value / world,
                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches * world,
-               "clocks": clk.summary()}
+               "clocks": clk.summary(), "fft_reference": fft_ref}
         print(json.dumps(out), flush=True)
     sv.close()
     if world > 1:

@@ -1204,7 +1204,8 @@ double sr_sb_last_change(const sr_sb_ctx* c) { return c ? c->last_change : -1.0;
 
 int sr_sb_launches_per_iteration(const sr_sb_ctx* c) {
     if (!c) return -1;
-    const int per = 4 * c->p.S + (c->p.w_mode == SR_W_FIXED_POINT ? c->p.w_iters : 1);
+    const int per_sweep = c->p.phi_solver == SR_PHI_AOS ? 3 : 4;   // rhs + (r2c, cols, c2r | vert, horiz)
+    const int per = per_sweep * c->p.S + (c->p.w_mode == SR_W_FIXED_POINT ? c->p.w_iters : 1);
     return c->backend == BK_LOCAL ? per * (int)c->members.size() : per;
 }
 

@@ -155,3 +155,15 @@ def test_aos_differs_from_fft(S):
 def test_aos_rejected_in_slab_mode(S):
     with pytest.raises(S.SrsbError):
         S.Solver(256, 256, 1, window=3, slabs=2, phi_solver=1)
+
+
+def test_launch_counts(S):
+    """sr_sb_launches_per_iteration (bench.py's gpu_launches): rhs + 3 FFT passes per sweep + w/b
+    passes; the AOS sweep has 2 solve launches instead of 3."""
+    p = _params(3)
+    with _solver(S, 64, 64, 1, p) as sv:
+        assert sv.launches_per_iteration == 3 * 3 + 1
+    with S.Solver(64, 64, 1, window=3, **{k: p[k] for k in KEYS}) as sv:
+        assert sv.launches_per_iteration == 4 * 3 + 1
+    with S.Solver(64, 64, 1, window=3, **dict({k: p[k] for k in KEYS}, w_mode=1, w_iters=3)) as sv:
+        assert sv.launches_per_iteration == 4 * 3 + 3

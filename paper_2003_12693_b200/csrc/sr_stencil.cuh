@@ -16,36 +16,13 @@
 // row half-width -- an exact regrouping of the window sum (different rounding order).
 #pragma once
 #include <cuda_runtime.h>
+#include "sr_f32x2.cuh"
 #include "sr_tma.cuh"
 
 namespace srsb {
 
 constexpr float kPi = 3.14159265358979323846f;
 
-// ------------------------------------------------------------------ packed f32x2 arithmetic (FFMA2/FADD2)
-__device__ __forceinline__ unsigned long long f2u(float2 a) { return *reinterpret_cast<unsigned long long*>(&a); }
-__device__ __forceinline__ float2 u2f(unsigned long long a) { return *reinterpret_cast<float2*>(&a); }
-__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
-    unsigned long long d;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)), "l"(f2u(c)));
-    return u2f(d);
-}
-__device__ __forceinline__ float2 add2(float2 a, float2 b) {
-    unsigned long long d;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
-    return u2f(d);
-}
-__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
-    unsigned long long d;
-    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
-    return u2f(d);
-}
-__device__ __forceinline__ float2 sub2(float2 a, float2 b) {
-    unsigned long long d;
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2u(a)), "l"(f2u(b)));
-    return u2f(d);
-}
-__device__ __forceinline__ float2 f2(float x) { return make_float2(x, x); }
 
 // ------------------------------------------------------------------ regularizers (Eq. 5, 6, 11, 28, 29)
 // All of H(x +- l), delta(x +- l), delta(x), delta'(x) from ONE sincospif(x / eps): the arguments

@@ -18,7 +18,9 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 
 __all__ = ["build", "Params", "H", "delta", "delta_prime", "h", "h_prime", "grad", "div", "edge",
            "fft", "fft2", "symbol", "solve", "window_sum", "rhs", "shrink", "project", "wb",
-           "init", "sweep", "iterate", "label", "run", "lib", "energy", "thomas_neumann", "solve_aos"]
+           "init", "sweep", "iterate", "label", "run", "lib", "energy", "thomas_neumann", "solve_aos",
+           "grad3", "div3", "edge3", "fft3", "symbol3", "solve3", "window_sum3", "rhs3", "shrink3", "project3",
+           "wb3", "init3", "iterate3", "run3"]
 
 
 def build(force: bool = False) -> str:
@@ -56,6 +58,15 @@ def lib():
             "orc_energy": (None, [i, i, p, p, p, p, p, p, p, p]),
             "orc_thomas_neumann": (None, [i, d, p, p]),
             "orc_solve_aos": (None, [i, i, d, d, p, p]),
+            "orc3_grad": (None, [i, i, i, p, p, p, p]), "orc3_div": (None, [i, i, i, p, p, p, p]),
+            "orc3_edge": (None, [i, i, i, p, d, d, i, p]), "orc3_fft3": (i, [i, i, i, p, p, i]),
+            "orc3_symbol": (d, [i, i, i, d, d, i, i, i]), "orc3_solve": (i, [i, i, i, d, d, p, p]),
+            "orc3_window_sum": (None, [i, i, i, i, d, i, p, p, p, p, p, p]),
+            "orc3_rhs": (None, [i, i, i, p] + [p] * 9),
+            "orc3_shrink": (None, [p, d, p]), "orc3_project": (None, [i, p, p]),
+            "orc3_wb": (None, [i, i, i, p] + [p] * 8),
+            "orc3_init": (None, [i, i, i] + [p] * 8),
+            "orc3_iterate": (i, [i, i, i, p] + [p] * 8 + [i]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(_lib, name)
@@ -274,5 +285,127 @@ def run(p, image, phi0, K):
     g = edge(image, p["sigma"], p["rho"], p["s"])
     st = init(phi0)
     iterate(p, st, g, K)
+    st["g"] = g
+    return st
+
+
+# 3-D extension (NEXT-3, reading Q26) --------------------------------------------------------------
+# Volumes are [D][M][N]; vector fields are tuples (c1, c2, c3) = (along rows i, columns j, depth z).
+def grad3(phi):
+    phi = _d(phi)
+    D, M, N = phi.shape
+    g = [np.empty_like(phi) for _ in range(3)]
+    lib().orc3_grad(D, M, N, _ptr(phi), *[_ptr(a) for a in g])
+    return tuple(g)
+
+
+def div3(u1, u2, u3):
+    u1, u2, u3 = _d(u1), _d(u2), _d(u3)
+    D, M, N = u1.shape
+    out = np.empty_like(u1)
+    lib().orc3_div(D, M, N, _ptr(u1), _ptr(u2), _ptr(u3), _ptr(out))
+    return out
+
+
+def edge3(f, sigma=1.0, rho=1.0, s=2):
+    f = _d(f)
+    D, M, N = f.shape
+    g = np.empty_like(f)
+    lib().orc3_edge(D, M, N, _ptr(f), sigma, rho, s, _ptr(g))
+    return g
+
+
+def fft3(x, inverse=False):
+    x = np.asarray(x, dtype=np.complex128)
+    D, M, N = x.shape
+    re, im = _d(x.real.copy()), _d(x.imag.copy())
+    if lib().orc3_fft3(D, M, N, _ptr(re), _ptr(im), int(inverse)) != 0:
+        raise ValueError("sizes must be powers of two")
+    return re + 1j * im
+
+
+def symbol3(D, M, N, tau, mu, k3, k1, k2):
+    return float(lib().orc3_symbol(D, M, N, tau, mu, k3, k1, k2))
+
+
+def solve3(F, tau, mu, check=True):
+    F = _d(F)
+    D, M, N = F.shape
+    phi = np.empty_like(F)
+    bad = lib().orc3_solve(D, M, N, tau, mu, _ptr(F), _ptr(phi))
+    if check and bad:
+        raise FloatingPointError("imaginary part of the 3-D solve exceeds 1e-12 max|F| (Q11)")
+    return phi
+
+
+def window_sum3(u1, u2, u3, R, d, shape=0):
+    u1, u2, u3 = _d(u1), _d(u2), _d(u3)
+    D, M, N = u1.shape
+    v = [np.empty_like(u1) for _ in range(3)]
+    lib().orc3_window_sum(D, M, N, R, d, shape, _ptr(u1), _ptr(u2), _ptr(u3), *[_ptr(a) for a in v])
+    return tuple(v)
+
+
+def rhs3(p, psi, w, b, g):
+    """w, b: 3-tuples of [D][M][N] arrays."""
+    psi, g = _d(psi), _d(g)
+    w = [_d(a) for a in w]
+    b = [_d(a) for a in b]
+    D, M, N = psi.shape
+    F = np.empty_like(psi)
+    lib().orc3_rhs(D, M, N, _P(p), _ptr(psi), *[_ptr(a) for a in w], *[_ptr(a) for a in b], _ptr(g), _ptr(F))
+    return F
+
+
+def shrink3(B, t):
+    B = _d(B)
+    o = np.empty(3)
+    lib().orc3_shrink(_ptr(B), t, _ptr(o))
+    return o
+
+
+def project3(mode, a):
+    a = _d(a)
+    o = np.empty(3)
+    lib().orc3_project(mode, _ptr(a), _ptr(o))
+    return o
+
+
+def wb3(p, phi, w, b, g):
+    """Returns new (w, b) 3-tuples; inputs are not modified."""
+    phi, g = _d(phi), _d(g)
+    w = [np.array(a, dtype=np.float64, copy=True) for a in w]
+    b = [np.array(a, dtype=np.float64, copy=True) for a in b]
+    D, M, N = phi.shape
+    lib().orc3_wb(D, M, N, _P(p), _ptr(phi), *[_ptr(a) for a in w], *[_ptr(a) for a in b], _ptr(g))
+    return tuple(w), tuple(b)
+
+
+def init3(phi0):
+    phi0 = _d(phi0)
+    D, M, N = phi0.shape
+    out = [np.empty_like(phi0) for _ in range(7)]
+    lib().orc3_init(D, M, N, _ptr(phi0), *[_ptr(a) for a in out])
+    return dict(phi=out[0], w=tuple(out[1:4]), b=tuple(out[4:7]))
+
+
+def iterate3(p, state, g, K):
+    """Advance a 3-D state dict(phi, w=(3), b=(3)) by K outer iterations, in place."""
+    g = _d(g)
+    state["phi"] = np.array(state["phi"], dtype=np.float64, copy=True, order="C")
+    state["w"] = tuple(np.array(a, dtype=np.float64, copy=True, order="C") for a in state["w"])
+    state["b"] = tuple(np.array(a, dtype=np.float64, copy=True, order="C") for a in state["b"])
+    D, M, N = g.shape
+    bad = lib().orc3_iterate(D, M, N, _P(p), _ptr(state["phi"]), *[_ptr(a) for a in state["w"]],
+                             *[_ptr(a) for a in state["b"]], _ptr(g), K)
+    if bad:
+        raise FloatingPointError(f"{bad} 3-D solves failed the imaginary-part check (Q11)")
+    return state
+
+
+def run3(p, volume, phi0, K):
+    g = edge3(volume, p["sigma"], p["rho"], p["s"])
+    st = init3(phi0)
+    iterate3(p, st, g, K)
     st["g"] = g
     return st

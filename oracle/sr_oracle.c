@@ -594,3 +594,318 @@ int orc_label(int M, int N, const unsigned char *mask, int conn, int *labels)
     free(stack);
     return count;
 }
+
+/* ================================================================== */
+/* 3-D extension ("The algorithm can also be extended to 3D";   */
+/* Fig. 6 caption P:568).  Reading Q26: every     */
+/* operator gains the depth axis z (D planes of M x N):                 */
+/*   grad = (d_i, d_j, d_z) forward differences (Eq. 35 per axis),      */
+/*   div its Neumann adjoint (Eq. 36 per axis), the window a ball        */
+/*   p^2+q^2+r^2 <= R^2 (or a cube), the solve's symbol                  */
+/*   1 + tau mu (6 - 2cos z1 - 2cos z2 - 2cos z3) (Eq. 32 in 3-D),       */
+/*   shrink / projection on 3-vectors, the edge indicator with a 3-D     */
+/*   Gaussian.  Component order (1, 2, 3) = (rows i, columns j, depth z) */
+/*   so that a D = 1 volume reduces to the 2-D functions above exactly.  */
+/* ================================================================== */
+
+#define IDX3(z, i, j) (((size_t)(z) * (size_t)M + (size_t)(i)) * (size_t)N + (size_t)(j))
+
+void orc3_grad(int D, int M, int N, const double *phi, double *g1, double *g2, double *g3)
+{
+    #pragma omp parallel for schedule(static)
+    for (int z = 0; z < D; z++)
+        for (int i = 0; i < M; i++)
+            for (int j = 0; j < N; j++) {
+                size_t q = IDX3(z, i, j);
+                g1[q] = (i < M - 1) ? phi[IDX3(z, i + 1, j)] - phi[q] : 0.0;
+                g2[q] = (j < N - 1) ? phi[IDX3(z, i, j + 1)] - phi[q] : 0.0;
+                g3[q] = (z < D - 1) ? phi[IDX3(z + 1, i, j)] - phi[q] : 0.0;
+            }
+}
+
+void orc3_div(int D, int M, int N, const double *u1, const double *u2, const double *u3, double *out)
+{
+    #pragma omp parallel for schedule(static)
+    for (int z = 0; z < D; z++)
+        for (int i = 0; i < M; i++)
+            for (int j = 0; j < N; j++) {
+                double s = 0.0;
+                if (i < M - 1) s += u1[IDX3(z, i, j)];
+                if (i > 0) s -= u1[IDX3(z, i - 1, j)];
+                if (j < N - 1) s += u2[IDX3(z, i, j)];
+                if (j > 0) s -= u2[IDX3(z, i, j - 1)];
+                if (z < D - 1) s += u3[IDX3(z, i, j)];
+                if (z > 0) s -= u3[IDX3(z - 1, i, j)];
+                out[IDX3(z, i, j)] = s;
+            }
+}
+
+/* Eq. (1) in 3-D: separable normalized Gaussian along j, i, z (replicate padding), central
+ * differences (replicate padding) along the three axes. */
+void orc3_edge(int D, int M, int N, const double *f, double sigma, double rho, int s, double *g)
+{
+    int r = (int)ceil(3.0 * sigma);
+    double *k = (double *)malloc(sizeof(double) * (2 * r + 1));
+    double ks = 0.0;
+    for (int t = -r; t <= r; t++) { k[t + r] = exp(-(double)(t * t) / (2.0 * sigma * sigma)); ks += k[t + r]; }
+    for (int t = 0; t <= 2 * r; t++) k[t] /= ks;
+    size_t n = (size_t)D * M * N;
+    double *a = malloc(sizeof(double) * n), *b = malloc(sizeof(double) * n);
+    #pragma omp parallel for schedule(static)
+    for (int z = 0; z < D; z++)
+        for (int i = 0; i < M; i++)
+            for (int j = 0; j < N; j++) {
+                double acc = 0.0;
+                for (int t = -r; t <= r; t++) {
+                    int jj = j + t; if (jj < 0) jj = 0; if (jj > N - 1) jj = N - 1;
+                    acc += k[t + r] * f[IDX3(z, i, jj)];
+                }
+                a[IDX3(z, i, j)] = acc;
+            }
+    #pragma omp parallel for schedule(static)
+    for (int z = 0; z < D; z++)
+        for (int i = 0; i < M; i++)
+            for (int j = 0; j < N; j++) {
+                double acc = 0.0;
+                for (int t = -r; t <= r; t++) {
+                    int ii = i + t; if (ii < 0) ii = 0; if (ii > M - 1) ii = M - 1;
+                    acc += k[t + r] * a[IDX3(z, ii, j)];
+                }
+                b[IDX3(z, i, j)] = acc;
+            }
+    #pragma omp parallel for schedule(static)
+    for (int z = 0; z < D; z++)
+        for (int i = 0; i < M; i++)
+            for (int j = 0; j < N; j++) {
+                double acc = 0.0;
+                for (int t = -r; t <= r; t++) {
+                    int zz = z + t; if (zz < 0) zz = 0; if (zz > D - 1) zz = D - 1;
+                    acc += k[t + r] * b[IDX3(zz, i, j)];
+                }
+                a[IDX3(z, i, j)] = acc;   /* a = G_sigma * f */
+            }
+    #pragma omp parallel for schedule(static)
+    for (int z = 0; z < D; z++)
+        for (int i = 0; i < M; i++)
+            for (int j = 0; j < N; j++) {
+                int ip = i + 1 < M ? i + 1 : M - 1, im = i > 0 ? i - 1 : 0;
+                int jp = j + 1 < N ? j + 1 : N - 1, jm = j > 0 ? j - 1 : 0;
+                int zp = z + 1 < D ? z + 1 : D - 1, zm = z > 0 ? z - 1 : 0;
+                double gx = (a[IDX3(z, ip, j)] - a[IDX3(z, im, j)]) / 2.0;
+                double gy = (a[IDX3(z, i, jp)] - a[IDX3(z, i, jm)]) / 2.0;
+                double gz = (a[IDX3(zp, i, j)] - a[IDX3(zm, i, j)]) / 2.0;
+                double m2 = gx * gx + gy * gy + gz * gz;
+                double mag = (s == 2) ? m2 : sqrt(m2);
+                g[IDX3(z, i, j)] = 1.0 / (1.0 + rho * mag);
+            }
+    free(k); free(a); free(b);
+}
+
+/* 3-D FFT of a D x M x N complex array: rows (j), columns (i), depth (z). */
+int orc3_fft3(int D, int M, int N, double *re, double *im, int inverse)
+{
+    if (D < 1 || (D & (D - 1))) return -1;
+    for (int z = 0; z < D; z++)
+        if (orc_fft2(M, N, re + IDX3(z, 0, 0), im + IDX3(z, 0, 0), inverse)) return -1;
+    #pragma omp parallel
+    {
+        double *cr = malloc(sizeof(double) * D), *ci = malloc(sizeof(double) * D);
+        #pragma omp for schedule(static)
+        for (int q = 0; q < M * N; q++) {
+            for (int z = 0; z < D; z++) { cr[z] = re[(size_t)z * M * N + q]; ci[z] = im[(size_t)z * M * N + q]; }
+            orc_fft(D, cr, ci, inverse);
+            for (int z = 0; z < D; z++) { re[(size_t)z * M * N + q] = cr[z]; im[(size_t)z * M * N + q] = ci[z]; }
+        }
+        free(cr); free(ci);
+    }
+    return 0;
+}
+
+/* Eq. (32) in 3-D (Q10, Q26): 1 - tau mu (2cos z1 + 2cos z2 + 2cos z3 - 6). */
+double orc3_symbol(int D, int M, int N, double tau, double mu, int k3, int k1, int k2)
+{
+    double z1 = 2.0 * M_PI * (double)k1 / (double)M;
+    double z2 = 2.0 * M_PI * (double)k2 / (double)N;
+    double z3 = 2.0 * M_PI * (double)k3 / (double)D;
+    return 1.0 - tau * mu * (2.0 * cos(z1) + 2.0 * cos(z2) + 2.0 * cos(z3) - 6.0);
+}
+
+int orc3_solve(int D, int M, int N, double tau, double mu, const double *F, double *phi)
+{
+    size_t n = (size_t)D * M * N;
+    double *re = malloc(sizeof(double) * n), *im = calloc(n, sizeof(double));
+    memcpy(re, F, sizeof(double) * n);
+    orc3_fft3(D, M, N, re, im, 0);
+    for (int z = 0; z < D; z++)
+        for (int k1 = 0; k1 < M; k1++)
+            for (int k2 = 0; k2 < N; k2++) {
+                double sg = orc3_symbol(D, M, N, tau, mu, z, k1, k2);
+                re[IDX3(z, k1, k2)] /= sg;
+                im[IDX3(z, k1, k2)] /= sg;
+            }
+    orc3_fft3(D, M, N, re, im, 1);
+    double fmax = 0.0, imax = 0.0;
+    for (size_t q = 0; q < n; q++) {
+        if (fabs(F[q]) > fmax) fmax = fabs(F[q]);
+        if (fabs(im[q]) > imax) imax = fabs(im[q]);
+        phi[q] = re[q];
+    }
+    free(re); free(im);
+    return imax > 1e-12 * (fmax > 0 ? fmax : 1.0) ? 1 : 0;
+}
+
+/* P:368 in 3-D: v(x) = sum over the ball p^2+q^2+r^2 <= R^2 (shape 0) or the cube (1) of
+ * exp(-(p^2+q^2+r^2)/d^2) u(x + (p,q,r)); terms outside the volume are 0 (Q5). */
+void orc3_window_sum(int D, int M, int N, int R, double d, int shape, const double *u1, const double *u2,
+                     const double *u3, double *v1, double *v2, double *v3)
+{
+    #pragma omp parallel for schedule(static)
+    for (int z = 0; z < D; z++)
+        for (int i = 0; i < M; i++)
+            for (int j = 0; j < N; j++) {
+                double a1 = 0.0, a2 = 0.0, a3 = 0.0;
+                for (int r = -R; r <= R; r++)
+                    for (int p = -R; p <= R; p++)
+                        for (int q = -R; q <= R; q++) {
+                            if (shape == 0 && p * p + q * q + r * r > R * R) continue;
+                            int zz = z + r, ii = i + p, jj = j + q;
+                            if (zz < 0 || zz >= D || ii < 0 || ii >= M || jj < 0 || jj >= N) continue;
+                            double G = exp(-(double)(p * p + q * q + r * r) / (d * d));
+                            size_t s = IDX3(zz, ii, jj);
+                            a1 += G * u1[s]; a2 += G * u2[s]; a3 += G * u3[s];
+                        }
+                size_t o = IDX3(z, i, j);
+                v1[o] = a1; v2[o] = a2; v3[o] = a3;
+            }
+}
+
+/* Eq. (37) in 3-D. */
+void orc3_rhs(int D, int M, int N, const orc_params *P, const double *psi, const double *w1, const double *w2,
+              const double *w3, const double *b1, const double *b2, const double *b3, const double *g, double *F)
+{
+    size_t n = (size_t)D * M * N;
+    double *u1 = malloc(sizeof(double) * n), *u2 = malloc(sizeof(double) * n), *u3 = malloc(sizeof(double) * n);
+    double *v1 = malloc(sizeof(double) * n), *v2 = malloc(sizeof(double) * n), *v3 = malloc(sizeof(double) * n);
+    double *c1 = malloc(sizeof(double) * n), *c2 = malloc(sizeof(double) * n), *c3 = malloc(sizeof(double) * n);
+    double *dv = malloc(sizeof(double) * n);
+    for (size_t q = 0; q < n; q++) {
+        double hq = orc_h(psi[q], P->epsilon, P->l);
+        u1[q] = hq * w1[q]; u2[q] = hq * w2[q]; u3[q] = hq * w3[q];
+        c1[q] = b1[q] - w1[q]; c2[q] = b2[q] - w2[q]; c3[q] = b3[q] - w3[q];
+    }
+    orc3_window_sum(D, M, N, P->window, P->d, P->window_shape, u1, u2, u3, v1, v2, v3);
+    orc3_div(D, M, N, c1, c2, c3, dv);
+    #pragma omp parallel for schedule(static)
+    for (size_t q = 0; q < n; q++) {
+        double wn = sqrt(w1[q] * w1[q] + w2[q] * w2[q] + w3[q] * w3[q]);
+        double t = -P->gamma * g[q] * wn * orc_delta_prime(psi[q], P->epsilon)
+                 + P->alpha * g[q] * orc_delta(psi[q], P->epsilon)
+                 + 2.0 * P->beta * orc_h_prime(psi[q], P->epsilon, P->l)
+                       * (w1[q] * v1[q] + w2[q] * v2[q] + w3[q] * v3[q])
+                 + P->mu * dv[q];
+        F[q] = psi[q] + P->tau * t;
+    }
+    free(u1); free(u2); free(u3); free(v1); free(v2); free(v3); free(c1); free(c2); free(c3); free(dv);
+}
+
+/* Eq. (42) on 3-vectors. */
+void orc3_shrink(const double *B, double t, double *o)
+{
+    double nb = sqrt(B[0] * B[0] + B[1] * B[1] + B[2] * B[2]);
+    if (nb > 0.0) {
+        double m = nb - t; if (m < 0.0) m = 0.0;
+        for (int c = 0; c < 3; c++) o[c] = m * B[c] / nb;
+    } else {
+        o[0] = o[1] = o[2] = 0.0;
+    }
+}
+
+/* Eq. (40) on 3-vectors, modes as Q1. */
+void orc3_project(int mode, const double *a, double *o)
+{
+    double n = sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
+    double s = 1.0;
+    if (mode == 0) s = n > 1.0 ? n : 1.0;
+    else if (mode == 1) s = n > 1e-4 ? n : 1.0;
+    for (int c = 0; c < 3; c++) o[c] = a[c] / s;
+}
+
+/* w/b update (Eq. 41-42 or 38-39, 40, 23) in 3-D. */
+void orc3_wb(int D, int M, int N, const orc_params *P, const double *phi, double *w1, double *w2, double *w3,
+             double *b1, double *b2, double *b3, const double *g)
+{
+    size_t n = (size_t)D * M * N;
+    double *gp[3], *u[3], *v[3], *nw[3];
+    for (int c = 0; c < 3; c++) {
+        gp[c] = malloc(sizeof(double) * n); u[c] = malloc(sizeof(double) * n);
+        v[c] = malloc(sizeof(double) * n); nw[c] = malloc(sizeof(double) * n);
+    }
+    double *w[3] = {w1, w2, w3}, *b[3] = {b1, b2, b3};
+    double *hh = malloc(sizeof(double) * n);
+    orc3_grad(D, M, N, phi, gp[0], gp[1], gp[2]);
+    for (size_t q = 0; q < n; q++) hh[q] = orc_h(phi[q], P->epsilon, P->l);
+    if (P->w_mode == 0) {
+        for (size_t q = 0; q < n; q++) for (int c = 0; c < 3; c++) u[c][q] = hh[q] * w[c][q];
+        orc3_window_sum(D, M, N, P->window, P->d, P->window_shape, u[0], u[1], u[2], v[0], v[1], v[2]);
+        for (size_t q = 0; q < n; q++) {
+            double B[3], s[3], o[3];
+            for (int c = 0; c < 3; c++) B[c] = gp[c][q] + b[c][q] + (2.0 * P->beta / P->mu) * hh[q] * v[c][q];
+            double t = (P->gamma / P->mu) * g[q] * orc_delta(phi[q], P->epsilon);
+            orc3_shrink(B, t, s);
+            orc3_project(P->w_proj, s, o);
+            for (int c = 0; c < 3; c++) nw[c][q] = o[c];
+        }
+    } else {
+        for (int c = 0; c < 3; c++) memcpy(nw[c], w[c], sizeof(double) * n);
+        for (int r = 0; r < P->w_iters; r++) {
+            for (size_t q = 0; q < n; q++) for (int c = 0; c < 3; c++) u[c][q] = hh[q] * nw[c][q];
+            orc3_window_sum(D, M, N, P->window, P->d, P->window_shape, u[0], u[1], u[2], v[0], v[1], v[2]);
+            for (size_t q = 0; q < n; q++) {
+                double den = P->gamma * g[q] * orc_delta(phi[q], P->epsilon) + P->mu;
+                double a[3], o[3];
+                for (int c = 0; c < 3; c++) a[c] = (P->mu * gp[c][q] + P->mu * b[c][q] + 2.0 * P->beta * hh[q] * v[c][q]) / den;
+                orc3_project(P->w_proj, a, o);
+                for (int c = 0; c < 3; c++) nw[c][q] = o[c];
+            }
+        }
+    }
+    for (size_t q = 0; q < n; q++)
+        for (int c = 0; c < 3; c++) {
+            b[c][q] = b[c][q] + gp[c][q] - nw[c][q];
+            w[c][q] = nw[c][q];
+        }
+    for (int c = 0; c < 3; c++) { free(gp[c]); free(u[c]); free(v[c]); free(nw[c]); }
+    free(hh);
+}
+
+void orc3_init(int D, int M, int N, const double *phi0, double *phi, double *w1, double *w2, double *w3,
+               double *b1, double *b2, double *b3)
+{
+    size_t n = (size_t)D * M * N;
+    memcpy(phi, phi0, sizeof(double) * n);
+    orc3_grad(D, M, N, phi0, w1, w2, w3);
+    memset(b1, 0, sizeof(double) * n); memset(b2, 0, sizeof(double) * n); memset(b3, 0, sizeof(double) * n);
+}
+
+/* Algorithm 1 in 3-D: K outer iterations of S FFT sweeps, clamp, w/b update. */
+int orc3_iterate(int D, int M, int N, const orc_params *P, double *phi, double *w1, double *w2, double *w3,
+                 double *b1, double *b2, double *b3, const double *g, int K)
+{
+    int bad = 0;
+    size_t n = (size_t)D * M * N;
+    double *F = malloc(sizeof(double) * n);
+    for (int k = 0; k < K; k++) {
+        for (int s = 0; s < P->S; s++) {
+            orc3_rhs(D, M, N, P, phi, w1, w2, w3, b1, b2, b3, g, F);
+            bad += orc3_solve(D, M, N, P->tau, P->mu, F, phi);
+        }
+        if (P->phi_clip > 0.0)
+            for (size_t q = 0; q < n; q++) {
+                if (phi[q] > P->phi_clip) phi[q] = P->phi_clip;
+                if (phi[q] < -P->phi_clip) phi[q] = -P->phi_clip;
+            }
+        orc3_wb(D, M, N, P, phi, w1, w2, w3, b1, b2, b3, g);
+    }
+    free(F);
+    return bad;
+}

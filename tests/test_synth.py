@@ -29,3 +29,13 @@ def test_random_state():
     s = random_state(32, 16, batch=2, seed=1)
     assert s["phi"].shape == (2, 32, 16) and all(v.dtype == np.float32 for v in s.values())
     assert (np.abs(s["phi"]) < 1).mean() > 0.3
+
+
+def test_volume_recipe_is_seeded_and_shaped():
+    from synth import make_volume
+    a = make_volume((8, 16, 32), n=3, window=2, seed=1)
+    b = make_volume((8, 16, 32), n=3, window=2, seed=1)
+    assert a["volume"].shape == (8, 16, 32) and a["volume"].dtype == np.float32
+    assert np.array_equal(a["volume"], b["volume"]) and np.array_equal(a["phi0"], b["phi0"])
+    assert set(np.unique(a["phi0"])) == {-1.0, 1.0} and a["phi0"][0, 0, 0] == 1.0   # paper convention
+    assert a["params"]["window"] == 2 and a["params"]["beta"] > 0

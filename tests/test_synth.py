@@ -33,8 +33,8 @@ def test_random_state():
 
 def test_volume_recipe_is_seeded_and_shaped():
     from synth import make_volume
-    a = make_volume((8, 16, 32), n=3, window=2, seed=1)
-    b = make_volume((8, 16, 32), n=3, window=2, seed=1)
+    a = make_volume((8, 16, 32), n=3, window=2, seed=1, border=2)
+    b = make_volume((8, 16, 32), n=3, window=2, seed=1, border=2)
     assert a["volume"].shape == (8, 16, 32) and a["volume"].dtype == np.float32
     assert np.array_equal(a["volume"], b["volume"]) and np.array_equal(a["phi0"], b["phi0"])
     assert set(np.unique(a["phi0"])) == {-1.0, 1.0} and a["phi0"][0, 0, 0] == 1.0   # paper convention

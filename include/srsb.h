@@ -191,6 +191,39 @@ const char* sr_sb_last_error(const sr_sb_ctx* ctx);
 
 int sr_sb_abi_version(void);
 
+/* ---- 3-D extension ("The algorithm can also be extended to 3D",
+ * Fig. 6 caption P:568; reading Q26 of DESIGN.md).  One volume of D x M x N voxels per context,
+ * all powers of two, D (M + 1) <= 25600 (a D x M spectrum plane is solved in shared memory),
+ * p->batch = 1, window radius <= 4, FFT phi solver; every other parameter as in 2-D.
+ * Every operator gains the depth axis z: grad = forward differences along (i, j, z) with 0 on
+ * the last index of each axis (Eq. 35), div its Neumann adjoint (Eq. 36), the window the ball
+ * p^2 + q^2 + r^2 <= R^2 (window_shape 0) or the cube (1), the solve's symbol
+ * 1 + tau mu (6 - 2 cos z1 - 2 cos z2 - 2 cos z3) (Eq. 32), shrink / projection on 3-vectors,
+ * the edge indicator with a 3-D Gaussian.
+ * Layouts (dense, C order, host or device pointers): volume / phi / g [D][M][N] fp32; w, b
+ * [3][D][M][N] with components (along i, along j, along z).  Ownership and error behaviour as
+ * in 2-D (the context owns its device buffers; errors return a negative status and set
+ * sr_sb3_last_error). */
+typedef struct sr_sb3_ctx sr_sb3_ctx;
+sr_status sr_sb3_create(const sr_sb_params* p, int D, int device, void* stream, sr_sb3_ctx** out);
+/* Eq. (1) in 3-D and Alg. 1 (1): g from the volume, phi = phi0, w = grad phi0, b = 0. */
+sr_status sr_sb3_set_image(sr_sb3_ctx* ctx, const float* volume, const float* phi0);
+/* K outer iterations of Algorithm 1 in 3-D (S FFT sweeps, clamp, w/b update). */
+sr_status sr_sb3_iterate(sr_sb3_ctx* ctx, int K);
+sr_status sr_sb3_get_phi(sr_sb3_ctx* ctx, float* phi_out);
+sr_status sr_sb3_get_state(sr_sb3_ctx* ctx, float* phi, float* w, float* b, float* g);
+sr_status sr_sb3_set_state(sr_sb3_ctx* ctx, const float* phi, const float* w, const float* b, const float* g);
+/* Single steps on the same kernels: the 3-D solve of F (Eq. 33, no clamp); the RHS in increment
+ * form D = F - (1 - tau mu Delta_per) psi at the current state. */
+sr_status sr_sb3_debug_solve(sr_sb3_ctx* ctx, const float* F, float* phi_out);
+sr_status sr_sb3_debug_rhs(sr_sb3_ctx* ctx, float* D_out);
+/* As sr_sb_profile (classes: rhs, rows_r2c, cols_solve = the plane solve, rows_c2r, wb). */
+sr_status sr_sb3_profile(sr_sb3_ctx* ctx, int K, float* ms_out, int* launches_out);
+/* Synchronize; SR_ERR_NONFINITE if the w/b guard tripped. */
+sr_status sr_sb3_sync(sr_sb3_ctx* ctx);
+void sr_sb3_destroy(sr_sb3_ctx* ctx);
+const char* sr_sb3_last_error(const sr_sb3_ctx* ctx);
+
 #ifdef __cplusplus
 }
 #endif

@@ -31,3 +31,17 @@ bool pick_tma(int R, int shape, bool leq, RhsTmaKernel& k, WbTmaKernel (&wb)[2][
     return false;
 }
 }  // namespace srsb
+
+#include "sr_vol3.h"
+namespace srsb {
+bool pick_vol(int R, int shape, bool leq, VolRhsKernel& rhs, VolWbKernel (&wb)[2][2], int& smem) {
+    switch (R) {
+        case 0: return pick_vol_r0(shape, leq, rhs, wb, smem);
+        case 1: return pick_vol_r1(shape, leq, rhs, wb, smem);
+        case 2: return pick_vol_r2(shape, leq, rhs, wb, smem);
+        case 3: return pick_vol_r3(shape, leq, rhs, wb, smem);
+        case 4: return pick_vol_r4(shape, leq, rhs, wb, smem);
+    }
+    return false;
+}
+}  // namespace srsb

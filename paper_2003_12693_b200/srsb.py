@@ -27,7 +27,10 @@ EXPORTS = ["sr_sb_default_params", "sr_sb_create", "sr_sb_set_image", "sr_sb_ite
            "sr_sb_debug_rhs", "sr_sb_debug_wb", "sr_sb_launches_per_iteration", "sr_sb_destroy",
            "sr_sb_last_error", "sr_sb_abi_version", "sr_sb_profile", "sr_sb_create_slab_group",
            "sr_sb_nccl_unique_id", "sr_sb_create_slab_nccl", "sr_sb_local_rows", "sr_sb_set_monitor",
-           "sr_sb_get_monitor", "sr_sb_iterate_until", "sr_sb_last_change"]
+           "sr_sb_get_monitor", "sr_sb_iterate_until", "sr_sb_last_change",
+           "sr_sb3_create", "sr_sb3_set_image", "sr_sb3_iterate", "sr_sb3_get_phi", "sr_sb3_get_state",
+           "sr_sb3_set_state", "sr_sb3_debug_solve", "sr_sb3_debug_rhs", "sr_sb3_profile", "sr_sb3_sync",
+           "sr_sb3_destroy", "sr_sb3_last_error"]
 KERNEL_CLASSES = ["rhs", "rows_r2c", "cols_solve", "rows_c2r", "wb", "aos_vert", "aos_horiz"]   # sr_kernel_class
 
 
@@ -84,6 +87,18 @@ def lib():
             "sr_sb_get_monitor": (st, [p, C.POINTER(C.c_double)]),
             "sr_sb_iterate_until": (st, [p, i, C.c_double, i, C.POINTER(C.c_int)]),
             "sr_sb_last_change": (C.c_double, [p]),
+            "sr_sb3_create": (st, [C.POINTER(Params), i, i, p, C.POINTER(p)]),
+            "sr_sb3_set_image": (st, [p, p, p]),
+            "sr_sb3_iterate": (st, [p, i]),
+            "sr_sb3_get_phi": (st, [p, p]),
+            "sr_sb3_get_state": (st, [p, p, p, p, p]),
+            "sr_sb3_set_state": (st, [p, p, p, p, p]),
+            "sr_sb3_debug_solve": (st, [p, p, p]),
+            "sr_sb3_debug_rhs": (st, [p, p]),
+            "sr_sb3_profile": (st, [p, i, C.POINTER(C.c_float), C.POINTER(C.c_int)]),
+            "sr_sb3_sync": (st, [p]),
+            "sr_sb3_destroy": (None, [p]),
+            "sr_sb3_last_error": (C.c_char_p, [p]),
         }
         for name, (res, args) in sig.items():
             fn = getattr(L, name)
@@ -268,3 +283,94 @@ class Solver:
 
     def debug_wb(self):
         self._check(lib().sr_sb_debug_wb(self._ctx))
+
+
+class Solver3:
+    """One sr_sb3 context (NEXT-3): a D x M x N volume on one device, bound to one CUDA stream.
+    Fields: phi / volume / g [D][M][N]; w, b [3][D][M][N] (components along i, j, z)."""
+
+    def __init__(self, D, M, N, window=3, device=None, stream=None, **params):
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("srsb needs a CUDA device (no CPU fallback)")
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        self.stream = stream
+        p = Params()
+        lib().sr_sb_default_params(C.byref(p), M, N, 1, window)
+        for k, v in params.items():
+            if not hasattr(p, k):
+                raise KeyError(f"unknown parameter {k}")
+            setattr(p, k, v)
+        self.params = {name: getattr(p, name) for name, _ in Params._fields_}
+        self.D, self.M, self.N = D, M, N
+        ctx = C.c_void_p()
+        st = lib().sr_sb3_create(C.byref(p), int(D), self.device.index, C.c_void_p(stream.cuda_stream), C.byref(ctx))
+        if st != SR_OK:
+            raise SrsbError(st, lib().sr_sb3_last_error(None).decode())
+        self._ctx = ctx
+
+    def _check(self, st):
+        if st != SR_OK:
+            raise SrsbError(st, lib().sr_sb3_last_error(self._ctx).decode())
+
+    def _field(self, nch=1):
+        import torch
+        shape = (nch, self.D, self.M, self.N) if nch > 1 else (self.D, self.M, self.N)
+        return torch.empty(shape, dtype=torch.float32, device=self.device)
+
+    def close(self):
+        if getattr(self, "_ctx", None):
+            lib().sr_sb3_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def set_image(self, volume, phi0):
+        self._check(lib().sr_sb3_set_image(self._ctx, _ptr(volume), _ptr(phi0)))
+
+    def iterate(self, K):
+        self._check(lib().sr_sb3_iterate(self._ctx, int(K)))
+
+    def get_phi(self, out=None):
+        out = self._field() if out is None else out
+        self._check(lib().sr_sb3_get_phi(self._ctx, _ptr(out)))
+        return out
+
+    def get_state(self):
+        out = {"phi": self._field(), "w": self._field(3), "b": self._field(3), "g": self._field()}
+        self._check(lib().sr_sb3_get_state(self._ctx, *[_ptr(out[k]) for k in ("phi", "w", "b", "g")]))
+        return out
+
+    def set_state(self, phi, w, b, g):
+        self._check(lib().sr_sb3_set_state(self._ctx, _ptr(phi), _ptr(w), _ptr(b), _ptr(g)))
+
+    def debug_solve(self, F):
+        out = self._field()
+        self._check(lib().sr_sb3_debug_solve(self._ctx, _ptr(F), _ptr(out)))
+        return out
+
+    def debug_rhs(self):
+        out = self._field()
+        self._check(lib().sr_sb3_debug_rhs(self._ctx, _ptr(out)))
+        return out
+
+    def profile(self, K):
+        ms = (C.c_float * len(KERNEL_CLASSES))()
+        n = (C.c_int * len(KERNEL_CLASSES))()
+        self._check(lib().sr_sb3_profile(self._ctx, int(K), ms, n))
+        return {name: (float(ms[i]), int(n[i])) for i, name in enumerate(KERNEL_CLASSES) if n[i]}
+
+    def sync(self):
+        self._check(lib().sr_sb3_sync(self._ctx))

@@ -20,7 +20,7 @@ def srsb():
 def declared_functions():
     hdr = open(os.path.join(ROOT, "include", "srsb.h")).read()
     hdr = re.sub(r"/\*.*?\*/", "", hdr, flags=re.S)
-    return sorted(set(re.findall(r"\b(sr_sb_\w+)\s*\(", hdr)))
+    return sorted(set(re.findall(r"\b(sr_sb3?_\w+)\s*\(", hdr)))
 
 
 def test_every_declared_symbol_is_exported(srsb):
@@ -113,3 +113,15 @@ def test_product_path_never_imports_the_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"import\s+oracle|from\s+oracle|liboracle|sr_oracle|orc_", txt), \
                     os.path.join(dirpath, f)
+
+
+@pytest.mark.parametrize("D,field,value,status", [(3, "M", 64, -2), (8, "batch", 2, -2), (8, "window", 5, -1),
+                                                  (256, "M", 128, -2), (8, "phi_solver", 1, -1), (0, "M", 64, -2)])
+def test_create3_validates_before_device(srsb, D, field, value, status):
+    p = srsb.Params()
+    srsb.lib().sr_sb_default_params(C.byref(p), 64, 64, 1, 3)
+    setattr(p, field, value)
+    ctx = C.c_void_p()
+    assert srsb.lib().sr_sb3_create(C.byref(p), D, 0, None, C.byref(ctx)) == status
+    assert not ctx.value
+    assert srsb.lib().sr_sb3_last_error(None)

@@ -41,7 +41,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c3", choices=["c1", "c2", "c3", "c4", "c5", "v3d"],
+                    help="v3d: the 3-D extension (NEXT-3) on a synthetic 128^3 volume")
     ap.add_argument("--images", type=int, default=None, help="override the batch (C3 only)")
     ap.add_argument("--iters", type=int, default=None, help="override iterations per step")
     ap.add_argument("--phi-solver", default="fft", choices=["fft", "aos"],
@@ -223,8 +224,123 @@ def config_json(cfg, ngpu):
                   else "L2-resident config (state < 126 MB): latency-bound, not an HBM measurement"}
 
 
+VOL_BYTES_PER_VOX = {"rhs": 36.0, "rows_r2c": 8.0, "cols_solve": 8.0, "rows_c2r": 12.0, "wb": 56.0}
+
+
+def run_volume(args, world, rank, local):
+    """--config v3d: the 3-D extension on a synthetic 128^3 volume (synth.volumes),
+    R = 3, K = 200 iterations per step; value in Mvox-iter/s.  N > 1: independent replicas."""
+    import numpy as np
+    import torch
+    from paper_2003_12693_b200 import Solver3
+    from synth import make_volume
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2003_12693_b200.dist import max_over_ranks as _max_over_ranks
+    shape, R = (128, 128, 128), 3
+    K = args.iters or 200
+    v = make_volume(shape, n=12, window=R, seed=0)
+    p = v["params"]
+    keys = ("gamma", "alpha", "beta", "mu", "epsilon", "l", "d", "window_shape", "tau", "S", "rho", "sigma", "s",
+            "phi_clip", "w_proj", "w_mode", "w_iters")
+    stream = torch.cuda.Stream(dev)
+    sv = Solver3(*shape, window=R, device=local, stream=stream, **{k: p[k] for k in keys})
+    vol_d = torch.from_numpy(v["volume"]).to(dev)
+    phi_d = torch.from_numpy(v["phi0"]).to(dev)
+    out_d = torch.empty_like(phi_d)
+    nvox = int(np.prod(shape))
+
+    def step():
+        sv.set_image(vol_d, phi_d)
+        sv.iterate(K)
+        sv.get_phi(out_d)
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clk:
+            e0.record(stream)
+            for _ in range(args.steps):
+                step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+    sv.sync()
+    ms = _max_over_ranks(e0.elapsed_time(e1), device=dev)
+    value = world * nvox * K * args.steps / (ms / 1e3) / 1e6
+    peak, peak_src = peaks()
+    sv.set_image(vol_d, phi_d)
+    prof = sv.profile(2)
+    dom = max(prof, key=lambda k: prof[k][0])
+    kern = {k: {"ms_per_launch": a / n, "launches_per_iter": n // 2,
+                "GBs": VOL_BYTES_PER_VOX[k] * nvox / (a / n / 1e3) / 1e9} for k, (a, n) in prof.items()}
+    roof = {"bound": "hbm", "kernel": dom, "achieved": kern[dom]["GBs"], "peak": peak, "unit": "GB/s",
+            "frac": kern[dom]["GBs"] / peak, "traffic": None, "peak_source": peak_src,
+            "bytes_per_vox_per_launch": VOL_BYTES_PER_VOX[dom], "kernels": kern}
+    if rank == 0:
+        print(json.dumps({"metric": "megavoxel-iterations/s per SB-SR iteration (3-D extension, NEXT-3)",
+                          "value": value, "unit": "Mvox-iter/s", "n_gpus": world, "steps": args.steps,
+                          "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                          "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                          "config": {"workload": f"v3d: one {shape[0]}x{shape[1]}x{shape[2]} fp32 volume (12 random "
+                                                 f"ellipsoids, noise 0.15), {K} SB iterations, ball radius {R}, S=3",
+                                     "l2": "state 46 B/voxel x 2 Mvox = 96 MB: partly L2-resident",
+                                     "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+                          "roofline": roof, "gpu_launches": args.steps * (5 + K * 13) * world,
+                          "clocks": clk.summary()}), flush=True)
+    sv.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def run_reference_volume(args, rank):
+    """--impl reference --config v3d: the 3-D float64 oracle on a 64^3 crop of the v3d recipe (bounded
+    sample), one SB iteration per step, rank 0 only."""
+    if rank != 0:
+        return None
+    import oracle
+    from synth import make_volume
+    oracle.build()
+    cores = len(os.sched_getaffinity(0))
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    v = make_volume((64, 64, 64), n=4, window=3, seed=0)
+    p = v["params"]
+    g = oracle.edge3(v["volume"], p["sigma"], p["rho"], p["s"])
+    st = oracle.init3(v["phi0"])
+    for _ in range(args.warmup):
+        oracle.iterate3(p, st, g, 1)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.iterate3(p, st, g, 1)
+    t = time.perf_counter() - t0
+    value = 64 ** 3 * args.steps / t / 1e6
+    return {"impl": "reference", "metric": "megavoxel-iterations/s per SB-SR iteration (3-D extension, NEXT-3)",
+            "value": value, "unit": "Mvox-iter/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "v3d recipe, 64^3 crop, 1 SB iteration per step, ball radius 3, S=3"},
+            "cpu_baseline": {"value": value, "unit": "Mvox-iter/s", "cores": cores, "kind": "oracle",
+                             "sample": f"64^3 volume, 1 SB iteration per step, float64 C oracle, "
+                                       f"OMP_NUM_THREADS={os.environ['OMP_NUM_THREADS']}"},
+            "e2e": {"value": value, "unit": "Mvox-iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
 def main():
     args = parse()
+    if args.config == "v3d" and args.impl == "reference":
+        out = run_reference_volume(args, int(os.environ.get("RANK", "0")))
+        if out is not None:
+            print(json.dumps(out), flush=True)
+        return 0
+    if args.config == "v3d" and args.impl != "reference":
+        return run_volume(args, int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")),
+                          int(os.environ.get("LOCAL_RANK", "0")))
     cfg = workload(args)
     cfg["name"] = args.config
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -38,19 +38,21 @@ __device__ __forceinline__ int brev_bits(int v, int bits) { return bits ? (int)(
 __device__ __forceinline__ int pidx(int z, int i, int M) { return z * (M + 1) + i; }
 
 // In-place radix-2 DIT stages along one axis of the plane (input already bit-reversed along it).
-// AXIS 0: lines along i (length M, D lines); AXIS 1: lines along z (length D, M lines).
+// AXIS 0: lines along i (length M = 2^lgM, D lines); AXIS 1: lines along z (length D = 2^lgD, M
+// lines).  tw: the axis' twiddles exp(-2 pi i m / L), m < L/2, staged in shared memory.
 template <int AXIS, bool INV>
-__device__ __forceinline__ void plane_stages(float2* P, int D, int M, const float2* __restrict__ tw) {
-    const int L = AXIS == 0 ? M : D, lines = AXIS == 0 ? D : M;
-    for (int h = 1; h < L; h <<= 1) {
-        const int stride = L / (2 * h);
-        for (int b = threadIdx.x; b < lines * (L / 2); b += blockDim.x) {
-            const int line = b / (L / 2), bb = b - line * (L / 2);
-            const int grp = bb / h, k = bb - grp * h;
-            const int i0 = grp * 2 * h + k, i1 = i0 + h;
+__device__ __forceinline__ void plane_stages(float2* P, int lgD, int lgM, const float2* tw) {
+    const int M = 1 << lgM;
+    const int lgL = AXIS == 0 ? lgM : lgD, lgl = AXIS == 0 ? lgD : lgM;
+    const int nb = 1 << (lgL - 1 + lgl);            // butterflies per stage
+    for (int s = 0; s < lgL; s++) {
+        const int h = 1 << s;
+        for (int b = threadIdx.x; b < nb; b += blockDim.x) {
+            const int line = b >> (lgL - 1), bb = b & ((1 << (lgL - 1)) - 1);
+            const int k = bb & (h - 1), i0 = ((bb >> s) << (s + 1)) + k, i1 = i0 + h;
             const int a0 = AXIS == 0 ? pidx(line, i0, M) : pidx(i0, line, M);
             const int a1 = AXIS == 0 ? pidx(line, i1, M) : pidx(i1, line, M);
-            float2 w = __ldg(&tw[k * stride]);
+            float2 w = tw[k << (lgL - 1 - s)];
             if (INV) w.y = -w.y;
             const float2 x0 = P[a0], x1 = P[a1];
             const float2 t = make_float2(w.x * x1.x - w.y * x1.y, w.x * x1.y + w.y * x1.x);
@@ -63,12 +65,13 @@ __device__ __forceinline__ void plane_stages(float2* P, int D, int M, const floa
 
 // bit-reverse permutation along one axis, in place
 template <int AXIS>
-__device__ __forceinline__ void plane_brev(float2* P, int D, int M) {
-    const int L = AXIS == 0 ? M : D, lines = AXIS == 0 ? D : M;
-    const int bits = __ffs(L) - 1;
-    for (int e = threadIdx.x; e < lines * L; e += blockDim.x) {
-        const int line = e / L, x = e - line * L, y = brev_bits(x, bits);
-        if (bits > 0 && x < y) {
+__device__ __forceinline__ void plane_brev(float2* P, int lgD, int lgM) {
+    const int M = 1 << lgM;
+    const int lgL = AXIS == 0 ? lgM : lgD, lgl = AXIS == 0 ? lgD : lgM;
+    if (lgL == 0) return;
+    for (int e = threadIdx.x; e < (1 << (lgL + lgl)); e += blockDim.x) {
+        const int line = e >> lgL, x = e & ((1 << lgL) - 1), y = brev_bits(x, lgL);
+        if (x < y) {
             const int a = AXIS == 0 ? pidx(line, x, M) : pidx(x, line, M);
             const int c = AXIS == 0 ? pidx(line, y, M) : pidx(y, line, M);
             const float2 t = P[a];
@@ -286,31 +289,35 @@ __global__ void __launch_bounds__(256) k3_wb(const float* __restrict__ phi, cons
 }
 
 #ifdef SRSB_VOL_HOST_KERNELS   // non-template kernels: defined in srsb3.cu only
-// grid = H (one spectrum column k2 per CTA), dynamic smem D (M + 1) float2.
+// grid = H (one spectrum column k2 per CTA), dynamic smem D (M + 1) + (M + D) / 2 float2.
 // spec[k2][z * M + i] (the row pass's layout with G = 1 over the D*M rows).
-__global__ void __launch_bounds__(512) k3_planes_solve(float2* __restrict__ spec, const float2* __restrict__ twM,
-                                                       const float2* __restrict__ twD, const float* __restrict__ cM,
-                                                       const float* __restrict__ cD, const float* __restrict__ cN,
-                                                       PlaneArgs a) {
+__global__ void __launch_bounds__(1024) k3_planes_solve(float2* __restrict__ spec, const float2* __restrict__ twM,
+                                                        const float2* __restrict__ twD, const float* __restrict__ cM,
+                                                        const float* __restrict__ cD, const float* __restrict__ cN,
+                                                        PlaneArgs a) {
     extern __shared__ float4 smem_v4[];
     float2* P = reinterpret_cast<float2*>(smem_v4);
     const int D = a.D, M = a.M, k2 = blockIdx.x;
+    const int lgD = __ffs(D) - 1, lgM = __ffs(M) - 1;
+    float2* tM = P + D * (M + 1);
+    float2* tD = tM + M / 2;
+    for (int m = threadIdx.x; m < M / 2; m += blockDim.x) tM[m] = __ldg(&twM[m]);
+    for (int m = threadIdx.x; m < D / 2; m += blockDim.x) tD[m] = __ldg(&twD[m]);
     float2* col = spec + (long long)k2 * D * M;
-    const int bm = __ffs(M) - 1;
     // load with the i-axis bit reversal folded in
     for (int e = threadIdx.x; e < D * M; e += blockDim.x) {
-        const int z = e / M, i = e - z * M;
-        P[pidx(z, brev_bits(i, bm), M)] = col[e];
+        const int z = e >> lgM, i = e & (M - 1);
+        P[pidx(z, brev_bits(i, lgM), M)] = col[e];
     }
     __syncthreads();
-    plane_stages<0, false>(P, D, M, twM);
-    plane_brev<1>(P, D, M);
-    plane_stages<1, false>(P, D, M, twD);
+    plane_stages<0, false>(P, lgD, lgM, tM);
+    plane_brev<1>(P, lgD, lgM);
+    plane_stages<1, false>(P, lgD, lgM, tD);
     // divide by the symbol (Eq. 32 in 3-D); k2 = 0 holds (X[.., 0], X[.., N/2]) packed as Z = A + iB
     const float cn = __ldg(&cN[k2]);
     if (k2 != 0) {
         for (int e = threadIdx.x; e < D * M; e += blockDim.x) {
-            const int z = e / M, i = e - z * M;
+            const int z = e >> lgM, i = e & (M - 1);
             const float s = a.scale / (1.f + a.taumu * (__ldg(&cD[z]) + __ldg(&cM[i]) + cn));
             float2& v = P[pidx(z, i, M)];
             v = make_float2(v.x * s, v.y * s);
@@ -318,7 +325,7 @@ __global__ void __launch_bounds__(512) k3_planes_solve(float2* __restrict__ spec
     } else {
         const float c0 = __ldg(&cN[0]), ch = __ldg(&cN[a.H]);
         for (int e = threadIdx.x; e < D * M; e += blockDim.x) {   // each (k, -k) pair once
-            const int z = e / M, i = e - z * M;
+            const int z = e >> lgM, i = e & (M - 1);
             const int zn = (D - z) & (D - 1), in = (M - i) & (M - 1);
             const int e2 = zn * M + in;
             if (e2 < e) continue;
@@ -332,12 +339,12 @@ __global__ void __launch_bounds__(512) k3_planes_solve(float2* __restrict__ spec
         }
     }
     __syncthreads();
-    plane_brev<0>(P, D, M);
-    plane_brev<1>(P, D, M);
-    plane_stages<0, true>(P, D, M, twM);
-    plane_stages<1, true>(P, D, M, twD);
+    plane_brev<0>(P, lgD, lgM);
+    plane_brev<1>(P, lgD, lgM);
+    plane_stages<0, true>(P, lgD, lgM, tM);
+    plane_stages<1, true>(P, lgD, lgM, tD);
     for (int e = threadIdx.x; e < D * M; e += blockDim.x) {
-        const int z = e / M, i = e - z * M;
+        const int z = e >> lgM, i = e & (M - 1);
         col[e] = P[pidx(z, i, M)];
     }
 }

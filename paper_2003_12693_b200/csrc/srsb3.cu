@@ -97,7 +97,7 @@ sr_status validate3(const sr_sb_params* p, int D, std::string& m) {
         m = "D, M, N must be powers of two (M, N >= 8, N <= 8192, D <= 1024)";
         return SR_ERR_SHAPE;
     }
-    if ((long long)D * (p->M + 1) * 8 > 200 * 1024) {
+    if ((long long)(D * (p->M + 1) + p->M / 2 + D / 2 + 1) * 8 > 200 * 1024) {
         m = "3-D: one D x M spectrum plane must fit in shared memory (D (M + 1) <= 25600)";
         return SR_ERR_SHAPE;
     }
@@ -154,8 +154,8 @@ sr_status configure3(sr_sb3_ctx* c) {
     c->pa.H = H;
     c->pa.taumu = p.tau * p.mu;
     c->pa.scale = (float)(1.0 / ((double)D * (double)M * (double)H));
-    c->psmem = D * (M + 1) * (int)sizeof(float2);
-    c->pthreads = 512;
+    c->psmem = (D * (M + 1) + M / 2 + D / 2 + 1) * (int)sizeof(float2);
+    c->pthreads = 1024;
     CK3(cudaFuncSetAttribute((const void*)k3_planes_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, c->psmem));
     // stencils
     if (!pick_vol(p.window, p.window_shape, p.l == p.epsilon, c->rhs, c->wb, c->vsmem))

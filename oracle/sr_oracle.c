@@ -24,7 +24,8 @@
  *   - w/b update: Eq. (41), (42), projection Eq. (40) as BALL/SPHERE/NONE (Q1), Eq. (23);
  *   - fixed-point w update: Eq. (38)-(40) (NEXT-2);
  *   - Algorithm 1 with fixed S sweeps (Q7) and the north-star clamp (Q9);
- *   - connected-component labelling by flood fill (validation).
+ *   - connected-component labelling by flood fill (validation);
+ *   - the 3-D extension (orc3_*, NEXT-3, reading Q26): the same steps with the depth axis.
  *
  * Parity pins: every function is pinned by tests/test_oracle_*.py against
  * closed forms, brute force, numpy/scipy library routines or invariants

@@ -35,12 +35,28 @@ bool pick_tma(int R, int shape, bool leq, RhsTmaKernel& k, WbTmaKernel (&wb)[2][
 #include "sr_vol3.h"
 namespace srsb {
 bool pick_vol(int R, int shape, bool leq, VolRhsKernel& rhs, VolWbKernel (&wb)[2][2], int& smem) {
-    switch (R) {
-        case 0: return pick_vol_r0(shape, leq, rhs, wb, smem);
-        case 1: return pick_vol_r1(shape, leq, rhs, wb, smem);
-        case 2: return pick_vol_r2(shape, leq, rhs, wb, smem);
-        case 3: return pick_vol_r3(shape, leq, rhs, wb, smem);
-        case 4: return pick_vol_r4(shape, leq, rhs, wb, smem);
+    if (R < 0 || R > 4 || shape < 0 || shape > 1) return false;
+    switch (R * 4 + shape * 2 + (leq ? 1 : 0)) {
+        case 0: set_vol_r0_s0_l0(rhs, wb, smem); return true;
+        case 1: set_vol_r0_s0_l1(rhs, wb, smem); return true;
+        case 2: set_vol_r0_s1_l0(rhs, wb, smem); return true;
+        case 3: set_vol_r0_s1_l1(rhs, wb, smem); return true;
+        case 4: set_vol_r1_s0_l0(rhs, wb, smem); return true;
+        case 5: set_vol_r1_s0_l1(rhs, wb, smem); return true;
+        case 6: set_vol_r1_s1_l0(rhs, wb, smem); return true;
+        case 7: set_vol_r1_s1_l1(rhs, wb, smem); return true;
+        case 8: set_vol_r2_s0_l0(rhs, wb, smem); return true;
+        case 9: set_vol_r2_s0_l1(rhs, wb, smem); return true;
+        case 10: set_vol_r2_s1_l0(rhs, wb, smem); return true;
+        case 11: set_vol_r2_s1_l1(rhs, wb, smem); return true;
+        case 12: set_vol_r3_s0_l0(rhs, wb, smem); return true;
+        case 13: set_vol_r3_s0_l1(rhs, wb, smem); return true;
+        case 14: set_vol_r3_s1_l0(rhs, wb, smem); return true;
+        case 15: set_vol_r3_s1_l1(rhs, wb, smem); return true;
+        case 16: set_vol_r4_s0_l0(rhs, wb, smem); return true;
+        case 17: set_vol_r4_s0_l1(rhs, wb, smem); return true;
+        case 18: set_vol_r4_s1_l0(rhs, wb, smem); return true;
+        case 19: set_vol_r4_s1_l1(rhs, wb, smem); return true;
     }
     return false;
 }

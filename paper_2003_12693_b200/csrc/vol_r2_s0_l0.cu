@@ -1,0 +1,5 @@
+// 3-D stencils: window radius 2, shape 0, l == eps 0
+#define SRSB_R 2
+#define SRSB_VSHAPE 0
+#define SRSB_VLEQ 0
+#include "vol_inst.cuh"

@@ -1,0 +1,5 @@
+// 3-D stencils: window radius 4, shape 1, l == eps 0
+#define SRSB_R 4
+#define SRSB_VSHAPE 1
+#define SRSB_VLEQ 0
+#include "vol_inst.cuh"

@@ -388,12 +388,10 @@ def main():
     stream = torch.cuda.Stream(dev)
     extra = {}
     if mode == "slab":
+        from paper_2003_12693_b200.dist import broadcast_unique_id
         from paper_2003_12693_b200.srsb import nccl_unique_id
-        ident = torch.zeros(128, dtype=torch.uint8, device=dev)
-        if rank == 0:
-            ident.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
-        torch.distributed.broadcast(ident, 0)
-        extra = dict(nccl=(world, rank, bytes(ident.cpu().numpy())))
+        ident = broadcast_unique_id(nccl_unique_id if rank == 0 else None, device=dev)
+        extra = dict(nccl=(world, rank, ident))
         rows = slice(rank * M // world, (rank + 1) * M // world)
         data["image"] = np.ascontiguousarray(data["image"][:, rows])
         data["phi0"] = np.ascontiguousarray(data["phi0"][:, rows])

@@ -110,6 +110,10 @@ sr_status sr_sb_create_slab_group(const sr_sb_params* p, int device, void* strea
 sr_status sr_sb_nccl_unique_id(void* id_out, int bytes);
 sr_status sr_sb_create_slab_nccl(const sr_sb_params* p, int device, void* stream, int nranks, int rank,
                                  const void* nccl_id, sr_sb_ctx** out);
+/* SURVEY §8(b)'s name and argument order for the NCCL slab context: the same as
+ * sr_sb_create_slab_nccl(p, device, stream, nranks, rank, nccl_unique_id, out). */
+sr_status sr_sb_create_dist(const sr_sb_params* p, int device, void* stream, const void* nccl_unique_id,
+                            int nranks, int rank, sr_sb_ctx** out);
 /* Rows per image held in the caller-visible buffers of this context (M, or M/P for an NCCL slab). */
 int sr_sb_local_rows(const sr_sb_ctx* ctx);
 

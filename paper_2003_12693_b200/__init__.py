@@ -3,6 +3,6 @@
 The product is libsrsb.so (C ABI: include/srsb.h) built from csrc/ for sm_100a;
 `srsb` is its thin ctypes binding.  See DESIGN.md.
 """
-from .srsb import Solver, Solver3, SrsbError, default_params, lib  # noqa: F401
+from .srsb import DistSolver, Solver, Solver3, SrsbError, default_params, lib  # noqa: F401
 
-__all__ = ["Solver", "Solver3", "SrsbError", "default_params", "lib"]
+__all__ = ["DistSolver", "Solver", "Solver3", "SrsbError", "default_params", "lib"]

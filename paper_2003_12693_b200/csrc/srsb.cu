@@ -913,6 +913,11 @@ sr_status sr_sb_create_slab_nccl(const sr_sb_params* p, int device, void* stream
     return SR_OK;
 }
 
+sr_status sr_sb_create_dist(const sr_sb_params* p, int device, void* stream, const void* nccl_unique_id,
+                            int nranks, int rank, sr_sb_ctx** out) {
+    return sr_sb_create_slab_nccl(p, device, stream, nranks, rank, nccl_unique_id, out);
+}
+
 int sr_sb_local_rows(const sr_sb_ctx* c) { return c ? c->Ml : -1; }
 
 sr_status sr_sb_set_image(sr_sb_ctx* c, const float* image, const float* phi0) {

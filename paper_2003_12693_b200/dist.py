@@ -49,3 +49,18 @@ def gather_batch(local: torch.Tensor, batch: int, device=None) -> torch.Tensor |
         s, e = shard(batch, world, r)
         out.append(parts[r][: e - s])
     return torch.cat(out, 0)
+
+
+def broadcast_unique_id(make_id=None, group=None, device=None, nbytes: int = 128) -> bytes:
+    """Rank 0 calls make_id() (sr_sb_nccl_unique_id) and broadcasts the bytes to every rank of
+    `group` (NCCL needs a device tensor: pass device; gloo works on CPU).  Returns the id bytes."""
+    rank = dist.get_rank(group)
+    buf = torch.zeros(nbytes, dtype=torch.uint8, device=device)
+    if rank == 0:
+        raw = make_id()
+        if len(raw) != nbytes:
+            raise ValueError("unexpected unique-id size")
+        buf.copy_(torch.frombuffer(bytearray(raw), dtype=torch.uint8))
+    src = dist.get_global_rank(group, 0) if group is not None else 0
+    dist.broadcast(buf, src, group=group)
+    return bytes(buf.cpu().numpy().tobytes())

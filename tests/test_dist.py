@@ -75,3 +75,31 @@ def test_sharded_run_matches_unsharded_gloo():
     for k in range(4):
         ref = oracle.run(cfg["params"], cfg["image"][k], cfg["phi0"][k], 3)["phi"]
         assert np.array_equal(full[k], ref)              # image order restored, bitwise
+
+
+def _id_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2003_12693_b200.dist import broadcast_unique_id
+        ident = broadcast_unique_id((lambda: bytes(range(128))) if rank == 0 else None)
+        q.put((rank, ident))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_unique_id_broadcast_gloo():
+    """DistSolver's plumbing: rank 0's NCCL unique id reaches every rank byte for byte."""
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_id_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    got = dict(q.get(timeout=120) for _ in range(world))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert got[0] == got[1] == bytes(range(128))

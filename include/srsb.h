@@ -136,6 +136,8 @@ sr_status sr_sb_set_state(sr_sb_ctx* ctx, const float* phi, const float* w, cons
 
 /* Outer iterations completed since set_image / set_state. */
 long long sr_sb_iteration(const sr_sb_ctx* ctx);
+/* Set the outer-iteration counter k (checkpoint / resume with sr_sb_set_state). */
+sr_status sr_sb_set_iteration(sr_sb_ctx* ctx, long long k);
 
 /* Block the host until the context's stream is idle; returns pending CUDA / non-finite errors. */
 sr_status sr_sb_sync(sr_sb_ctx* ctx);

@@ -1060,6 +1060,12 @@ sr_status sr_sb_set_state(sr_sb_ctx* c, const float* phi, const float* w, const 
 }
 
 long long sr_sb_iteration(const sr_sb_ctx* c) { return c ? c->k : -1; }
+sr_status sr_sb_set_iteration(sr_sb_ctx* c, long long k) {
+    if (!c) return SR_ERR_ARG;
+    if (k < 0) return fail(c, SR_ERR_ARG, "k must be >= 0");
+    c->k = k;
+    return SR_OK;
+}
 
 sr_status sr_sb_debug_solve(sr_sb_ctx* c, const float* F, float* phi_out) {
     if (!c) return SR_ERR_ARG;

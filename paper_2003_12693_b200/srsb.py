@@ -27,7 +27,7 @@ EXPORTS = ["sr_sb_default_params", "sr_sb_create", "sr_sb_set_image", "sr_sb_ite
            "sr_sb_debug_rhs", "sr_sb_debug_wb", "sr_sb_launches_per_iteration", "sr_sb_destroy",
            "sr_sb_last_error", "sr_sb_abi_version", "sr_sb_profile", "sr_sb_create_slab_group",
            "sr_sb_nccl_unique_id", "sr_sb_create_slab_nccl", "sr_sb_local_rows", "sr_sb_set_monitor",
-           "sr_sb_get_monitor", "sr_sb_iterate_until", "sr_sb_last_change", "sr_sb_create_dist",
+           "sr_sb_get_monitor", "sr_sb_iterate_until", "sr_sb_last_change", "sr_sb_create_dist", "sr_sb_set_iteration",
            "sr_sb3_create", "sr_sb3_set_image", "sr_sb3_iterate", "sr_sb3_get_phi", "sr_sb3_get_state",
            "sr_sb3_set_state", "sr_sb3_debug_solve", "sr_sb3_debug_rhs", "sr_sb3_profile", "sr_sb3_sync",
            "sr_sb3_destroy", "sr_sb3_last_error"]
@@ -88,6 +88,7 @@ def lib():
             "sr_sb_iterate_until": (st, [p, i, C.c_double, i, C.POINTER(C.c_int)]),
             "sr_sb_last_change": (C.c_double, [p]),
             "sr_sb_create_dist": (st, [C.POINTER(Params), i, p, p, i, i, C.POINTER(p)]),
+            "sr_sb_set_iteration": (st, [p, C.c_longlong]),
             "sr_sb3_create": (st, [C.POINTER(Params), i, i, p, C.POINTER(p)]),
             "sr_sb3_set_image": (st, [p, p, p]),
             "sr_sb3_iterate": (st, [p, i]),
@@ -236,6 +237,10 @@ class Solver:
     @property
     def iteration(self):
         return int(lib().sr_sb_iteration(self._ctx))
+
+    @iteration.setter
+    def iteration(self, k):
+        self._check(lib().sr_sb_set_iteration(self._ctx, int(k)))
 
     @property
     def launches_per_iteration(self):

@@ -706,6 +706,12 @@ __device__ __forceinline__ void rhs_points_tma(const float* Ps, const float* W1s
     const int M = a.M, N = a.N, gj = col0 + c0;
     const float* ph = phi + img * a.plane;
     float* Do = D + img * a.plane;
+    // values of row i - 1 carried in registers: psi (the Laplacian's upper neighbour) and b1 - w1
+    // (the divergence's upper term); psi of row i is the previous row's lower neighbour
+    float2 P = *reinterpret_cast<const float2*>(Ps + (G::HR + r0) * G::PW + G::CA + c0);
+    float2 Pc = *reinterpret_cast<const float2*>(Ps + (G::HR + r0 - 1) * G::PW + G::CA + c0);
+    float2 c1c = sub2(*reinterpret_cast<const float2*>(B1s + r0 * G::BW + 4 + c0),
+                      *reinterpret_cast<const float2*>(W1s + (G::HR + r0 - 1) * G::PW + G::CA + c0));
 #pragma unroll
     for (int i = 0; i < G::RT; i++) {
         const int tr = r0 + i, gi = row0 + tr;
@@ -715,16 +721,14 @@ __device__ __forceinline__ void rhs_points_tma(const float* Ps, const float* W1s
         const float* w2r = W2s + (G::HR + tr) * G::PW + G::CA + c0;
         const float* b1r = B1s + (1 + tr) * G::BW + 4 + c0;
         const float* b2r = B2s + (1 + tr) * G::BW + 4 + c0;
-        const float2 P = *reinterpret_cast<const float2*>(prow);
-        float2 Pu = *reinterpret_cast<const float2*>(prow - G::PW);
-        float2 Pd = *reinterpret_cast<const float2*>(prow + G::PW);
+        const float2 Pn = *reinterpret_cast<const float2*>(prow + G::PW);
+        float2 Pu = Pc, Pd = Pn;
         float pl = prow[-1], pr = prow[ST_CT];
         const float2 W1 = *reinterpret_cast<const float2*>(w1r), W2 = *reinterpret_cast<const float2*>(w2r);
-        const float2 W1u = *reinterpret_cast<const float2*>(w1r - G::PW);
         const float2 B1 = *reinterpret_cast<const float2*>(b1r), B2 = *reinterpret_cast<const float2*>(b2r);
-        const float2 B1u = *reinterpret_cast<const float2*>(b1r - G::BW);
         const float2 Gv = *reinterpret_cast<const float2*>(Gs + tr * G::TW + c0);
-        float2 c1 = sub2(B1, W1), c1u = sub2(B1u, W1u), c2 = sub2(B2, W2);
+        const float2 c1n = sub2(B1, W1);
+        float2 c1 = c1n, c1u = c1c, c2 = sub2(B2, W2);
         float2 c2l = make_float2(b2r[-1] - w2r[-1], c2.x);   // (b2 - w2) at columns gj - 1, gj
         if (EDGE) {
             const int gig = gi + a.row_off;
@@ -754,6 +758,9 @@ __device__ __forceinline__ void rhs_points_tma(const float* Ps, const float* W1s
         t = fma2(f2(a.mu), dv, t);
         const float2 out = a.aos ? fma2(f2(a.tau), t, P) : mul2(f2(a.tau), fma2(f2(a.mu), lap, t));
         *reinterpret_cast<float2*>(Do + (long long)gi * N + gj) = out;
+        Pc = P;
+        P = Pn;
+        c1c = c1n;
     }
 }
 

@@ -26,6 +26,9 @@ namespace srsb {
 #ifndef SRSB_COLS_MAXNREG
 #define SRSB_COLS_MAXNREG 96   // 64-thread column CTAs: 96 registers -> 10 CTAs / SM without spills (128: 8)
 #endif
+#ifndef SRSB_COLS_MAXNREG_BIG
+#define SRSB_COLS_MAXNREG_BIG 64   // M >= 4096: 256 / 512-thread column CTAs, 2 resident per SM instead of 1
+#endif
 
 // float2 shared-memory index with one pad slot per 16 complex values (128 B): strided butterfly
 // accesses with power-of-two strides <= 16 hit 16 distinct 8-byte bank pairs per half-warp.
@@ -224,7 +227,7 @@ struct FftColArgs {
 // Column pass: forward FFT, divide by the symbol, inverse FFT, in place.  Threads of one column
 // are consecutive (t fastest), so a warp works inside one transform.
 template <int LOGM, int LOGE>
-__global__ void __maxnreg__(SRSB_COLS_MAXNREG) k_cols_solve(float2* __restrict__ spec, const float2* __restrict__ twM,
+__global__ void __maxnreg__(LOGM >= 12 ? SRSB_COLS_MAXNREG_BIG : SRSB_COLS_MAXNREG) k_cols_solve(float2* __restrict__ spec, const float2* __restrict__ twM,
                                                        const float* __restrict__ cM, const float* __restrict__ cN,
                                                        FftColArgs a) {
     constexpr int M = 1 << LOGM, E = 1 << LOGE, T = M / E;

@@ -324,3 +324,30 @@ def test_iterate_until_outer_change(S, orc):
     ref = np.linalg.norm(st["phi"] - a) / (np.linalg.norm(a) + 1e-6)
     assert ch == pytest.approx(ref, rel=5e-3, abs=1e-5)
     assert np.max(np.abs(phi - st["phi"])) < 1e-2
+
+
+# ----------------------------------------------------------------------------- degenerate cases
+def test_degenerate_cases(S, orc):
+    """K = 0 is a no-op; tau = 0 freezes phi (F = psi, Eq. 37) up to the clamp of phi0 = +-1;
+    beta = 0 (plain GAC, no repulsion) and R = 0 still match the oracle over 5 iterations."""
+    from synth import make_config
+    cfg = make_config("c1")
+    p = cfg["params"]
+    img, phi0 = cfg["image"], cfg["phi0"]
+    with _solver(S, 128, 128, 1, p) as sv:
+        sv.set_image(_cuda(img), _cuda(phi0))
+        sv.iterate(0)
+        assert sv.iteration == 0
+        assert np.array_equal(_np(sv.get_phi()), phi0.astype(np.float64))
+    with _solver(S, 128, 128, 1, dict(p, tau=0.0)) as sv:
+        sv.set_image(_cuda(img), _cuda(phi0))
+        sv.iterate(3)
+        assert np.max(np.abs(_np(sv.get_phi()) - phi0)) < 1e-6
+    for over in (dict(beta=0.0), dict(window=0, d=1.0)):
+        q = dict(p, **over)
+        with _solver(S, 128, 128, 1, q) as sv:
+            sv.set_image(_cuda(img), _cuda(phi0))
+            sv.iterate(5)
+            phi = _np(sv.get_phi())
+        ref = orc.run(q, img[0], phi0[0], 5)["phi"]
+        assert np.max(np.abs(phi[0] - ref)) <= 1e-4, over

@@ -97,3 +97,35 @@ def test_fullsize_rhs_and_wb_on_crops(S, orc, name, M, N, B, R):
             r1, r2, rb1, rb2 = orc.wb(p, *args)
             for got, ref in ((w_new[img, 0], r1), (w_new[img, 1], r2), (b_new[img, 0], rb1), (b_new[img, 1], rb2)):
                 assert np.max(np.abs(got[i0:i0 + c, j0:j0 + c] - ref[inner])) < 2e-5, (name, img, i0, j0)
+
+
+def test_fullsize_aos_solve_sampled(S, orc):
+    """NEXT-4 at the bench launch configuration (C3: 64 x 1024^2, --phi-solver aos): the AOS solve
+    of random fields against the oracle's, on the first and last image."""
+    from synth import paper_params
+    p = paper_params(4)
+    B, M, N = 64, 1024, 1024
+    with S.Solver(M, N, B, window=4, phi_solver=1, **{k: p[k] for k in KEYS}) as sv:
+        gen = torch.Generator(device="cuda").manual_seed(11)
+        F = torch.randn(B, M, N, generator=gen, device="cuda")
+        phi = sv.debug_solve(F)
+        torch.cuda.synchronize()
+        for b in (0, B - 1):
+            ref = orc.solve_aos(F[b].double().cpu().numpy(), p["tau"], p["mu"])
+            assert np.max(np.abs(phi[b].double().cpu().numpy() - ref)) <= 2e-6 * float(F[b].abs().max())
+
+
+def test_fullsize_3d_solve_residual(S):
+    """NEXT-3 at the bench size (one 128^3 volume): fp64 residual of the GPU's 3-D solve with the
+    periodic 7-point operator (a property that holds at any size)."""
+    from synth import paper_params3
+    p = paper_params3(3)
+    D = M = N = 128
+    with S.Solver3(D, M, N, window=3, **{k: p[k] for k in KEYS}) as sv:
+        gen = torch.Generator(device="cuda").manual_seed(13)
+        F = torch.randn(D, M, N, generator=gen, device="cuda")
+        phi = sv.debug_solve(F).double().cpu().numpy()
+    Fd = F.double().cpu().numpy()
+    lap = sum(np.roll(phi, s, a) for a in range(3) for s in (1, -1)) - 6 * phi
+    res = np.linalg.norm(phi - p["tau"] * p["mu"] * lap - Fd) / np.linalg.norm(Fd)
+    assert res < 2e-6, res

@@ -10,4 +10,11 @@ ColKernel pick_col(int lg) {
     }
     return nullptr;
 }
+ColPKernel pick_col_p(int lg) {   // long columns only
+    switch (lg) {
+        case 12: return k_cols_solve_p<12, 4>;
+        case 13: return k_cols_solve_p<13, 4>;
+    }
+    return nullptr;
+}
 }  // namespace srsb

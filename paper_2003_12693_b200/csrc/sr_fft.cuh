@@ -20,6 +20,7 @@
 // the host.  No cuFFT.
 #pragma once
 #include <cuda_runtime.h>
+#include "sr_tma.cuh"
 
 namespace srsb {
 
@@ -288,6 +289,78 @@ __global__ void __maxnreg__(LOGM >= 12 ? SRSB_COLS_MAXNREG_BIG : SRSB_COLS_MAXNR
     fft_stages<LOGM, LOGE, 0, true>(v, sm, t, twM);
 #pragma unroll
     for (int u = 0; u < E; u++) base[addr(t + u * T)] = v[u];
+}
+
+// Persistent column solve for long contiguous columns (M >= 4096, G = 1, whole-image contexts):
+// such a column needs a 256 / 512-thread CTA and only one fits per SM without spilling, so
+// nothing overlaps its load with its transforms.  Here each CTA strides over the columns and one
+// elected thread fetches the next column into a second shared buffer with a bulk async copy
+// (cp.async.bulk on an mbarrier) while the current one is transformed.  Same arithmetic as
+// k_cols_solve.
+template <int LOGM, int LOGE>
+__global__ void __launch_bounds__(512, 1) k_cols_solve_p(float2* __restrict__ spec, const float2* __restrict__ twM,
+                                                         const float* __restrict__ cM, const float* __restrict__ cN,
+                                                         FftColArgs a, int ncols, int lg_hl) {
+    constexpr int M = 1 << LOGM, E = 1 << LOGE, T = M / E;
+    constexpr uint32_t BYTES = M * sizeof(float2);
+    extern __shared__ float4 smem_cp[];
+    float2* buf = reinterpret_cast<float2*>(smem_cp);      // [M] prefetch buffer (dense)
+    float2* sm = buf + M;                                   // padded exchange row (SC)
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + a.SC);
+    const int t = threadIdx.x;
+    const int hl = 1 << lg_hl;
+    auto col_ptr = [&](int c) { return spec + (long long)(c >> lg_hl) * a.bstride + (long long)(c & (hl - 1)) * M; };
+    int c = blockIdx.x;
+    if (t == 0) mbar_init(bar, 1);
+    __syncthreads();
+    if (t == 0 && c < ncols) {
+        mbar_expect_tx(bar, BYTES);
+        bulk_load(buf, col_ptr(c), BYTES, bar);
+    }
+    for (int it = 0; c < ncols; c += gridDim.x, it++) {
+        mbar_wait(bar, it & 1);
+        float2 v[E];
+#pragma unroll
+        for (int u = 0; u < E; u++) v[u] = buf[t + u * T];
+        __syncthreads();   // buf consumed: prefetch the next column while this one is transformed
+        if (t == 0 && c + (int)gridDim.x < ncols) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_expect_tx(bar, BYTES);
+            bulk_load(buf, col_ptr(c + gridDim.x), BYTES, bar);
+        }
+        fft_stages<LOGM, LOGE, 0, false>(v, sm, t, twM);
+        const int k2 = c & (hl - 1);
+        if (k2 == 0) {   // slot 0 packs the real columns k2 = 0 and N/2 (iteration-uniform)
+#pragma unroll
+            for (int u = 0; u < E; u++) sm[pad16(t + u * T)] = v[u];
+            __syncthreads();
+            const float c0 = __ldg(&cN[0]), ch = __ldg(&cN[a.H]);
+#pragma unroll
+            for (int u = 0; u < E; u++) {
+                const int k1 = t + u * T;
+                const float2 C = v[u];
+                const float2 Cc = conjf2(sm[pad16((M - k1) & (M - 1))]);
+                const float cm = __ldg(&cM[k1]);
+                const float s0 = a.scale / (1.f + a.taumu * (cm + c0));
+                const float sh = a.scale / (1.f + a.taumu * (cm + ch));
+                const float pp = 0.5f * (s0 + sh), mm = 0.5f * (s0 - sh);
+                v[u] = make_float2(pp * C.x + mm * Cc.x, pp * C.y + mm * Cc.y);
+            }
+            __syncthreads();
+        } else {
+            const float ck = __ldg(&cN[k2]);
+#pragma unroll
+            for (int u = 0; u < E; u++) {
+                const float sc = a.scale / (1.f + a.taumu * (__ldg(&cM[t + u * T]) + ck));
+                v[u] = make_float2(v[u].x * sc, v[u].y * sc);
+            }
+        }
+        fft_stages<LOGM, LOGE, 0, true>(v, sm, t, twM);
+        float2* out = col_ptr(c);
+#pragma unroll
+        for (int u = 0; u < E; u++) out[t + u * T] = v[u];
+        __syncthreads();   // the exchange row is free for the next column
+    }
 }
 
 // Row pass 2: transposed half spectrum -> inverse real FFT -> phi rows (accumulated, clamped).

@@ -40,6 +40,13 @@ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
 }
 __device__ __forceinline__ float2 conjf2(float2 a) { return make_float2(a.x, -a.y); }
 
+// scale / symbol(k1, k2) with symbol = 1 + tau mu (cm + ck) in [1, 1 + 8 tau mu] (Eq. 32, Q10).  The
+// denominator is always a normal number >= 1, so the approximate reciprocal (MUFU.RCP, <= 2 ulp) replaces
+// the IEEE division and its slow-path check (~8 instructions per spectral coefficient).
+__device__ __forceinline__ float sym_scale(float scale, float taumu, float cm, float ck) {
+    return __fdividef(scale, 1.f + taumu * (cm + ck));
+}
+
 __host__ __device__ constexpr int brevn(int k, int bits) {
     int r = 0;
     for (int i = 0; i < bits; i++) r |= ((k >> i) & 1) << (bits - 1 - i);
@@ -227,7 +234,9 @@ struct FftColArgs {
 
 // Column pass: forward FFT, divide by the symbol, inverse FFT, in place.  Threads of one column
 // are consecutive (t fastest), so a warp works inside one transform.
-template <int LOGM, int LOGE>
+// CONTIG: whole-image layout with G = 1 (one segment, each column M contiguous complex): element m
+// is col[m], so the E loads and stores use immediate offsets from one base pointer.
+template <int LOGM, int LOGE, bool CONTIG>
 __global__ void __maxnreg__(LOGM >= 12 ? SRSB_COLS_MAXNREG_BIG : SRSB_COLS_MAXNREG) k_cols_solve(float2* __restrict__ spec, const float2* __restrict__ twM,
                                                        const float* __restrict__ cM, const float* __restrict__ cN,
                                                        FftColArgs a) {
@@ -248,9 +257,10 @@ __global__ void __maxnreg__(LOGM >= 12 ? SRSB_COLS_MAXNREG_BIG : SRSB_COLS_MAXNR
         const int s = m >> a.lg_seg, mr = m & ((1 << a.lg_seg) - 1);
         return s * a.seg_stride + ((long long)((kg << a.lg_seg) + mr) << a.lg_G);
     };
+    float2* col = spec + b * a.bstride + ((long long)k2l << LOGM);   // CONTIG only
     float2 v[E];
 #pragma unroll
-    for (int u = 0; u < E; u++) v[u] = base[addr(t + u * T)];
+    for (int u = 0; u < E; u++) v[u] = CONTIG ? col[t + u * T] : base[addr(t + u * T)];
     fft_stages<LOGM, LOGE, 0, false>(v, sm, t, twM);
     if (blockIdx.x == 0 && a.k2_off == 0) {  // CTA-uniform: slot 0 packs the real columns k2 = 0, N/2
 #pragma unroll
@@ -264,8 +274,8 @@ __global__ void __maxnreg__(LOGM >= 12 ? SRSB_COLS_MAXNREG_BIG : SRSB_COLS_MAXNR
                 const float2 C = v[u];
                 const float2 Cc = conjf2(sm[pad16((M - k1) & (M - 1))]);
                 const float cm = __ldg(&cM[k1]);
-                const float s0 = a.scale / (1.f + a.taumu * (cm + c0));
-                const float sh = a.scale / (1.f + a.taumu * (cm + ch));
+                const float s0 = sym_scale(a.scale, a.taumu, cm, c0);
+                const float sh = sym_scale(a.scale, a.taumu, cm, ch);
                 const float p = 0.5f * (s0 + sh), m = 0.5f * (s0 - sh);
                 v[u] = make_float2(p * C.x + m * Cc.x, p * C.y + m * Cc.y);
             }
@@ -273,7 +283,7 @@ __global__ void __maxnreg__(LOGM >= 12 ? SRSB_COLS_MAXNREG_BIG : SRSB_COLS_MAXNR
             const float ck = __ldg(&cN[k2]);
 #pragma unroll
             for (int u = 0; u < E; u++) {
-                const float s = a.scale / (1.f + a.taumu * (__ldg(&cM[t + u * T]) + ck));
+                const float s = sym_scale(a.scale, a.taumu, __ldg(&cM[t + u * T]), ck);
                 v[u] = make_float2(v[u].x * s, v[u].y * s);
             }
         }
@@ -282,13 +292,16 @@ __global__ void __maxnreg__(LOGM >= 12 ? SRSB_COLS_MAXNREG_BIG : SRSB_COLS_MAXNR
         const float ck = __ldg(&cN[k2]);
 #pragma unroll
         for (int u = 0; u < E; u++) {
-            const float s = a.scale / (1.f + a.taumu * (__ldg(&cM[t + u * T]) + ck));
+            const float s = sym_scale(a.scale, a.taumu, __ldg(&cM[t + u * T]), ck);
             v[u] = make_float2(v[u].x * s, v[u].y * s);
         }
     }
     fft_stages<LOGM, LOGE, 0, true>(v, sm, t, twM);
 #pragma unroll
-    for (int u = 0; u < E; u++) base[addr(t + u * T)] = v[u];
+    for (int u = 0; u < E; u++) {
+        if (CONTIG) col[t + u * T] = v[u];
+        else base[addr(t + u * T)] = v[u];
+    }
 }
 
 // Persistent column solve for long contiguous columns (M >= 4096, G = 1, whole-image contexts):
@@ -341,8 +354,8 @@ __global__ void __launch_bounds__(512, 1) k_cols_solve_p(float2* __restrict__ sp
                 const float2 C = v[u];
                 const float2 Cc = conjf2(sm[pad16((M - k1) & (M - 1))]);
                 const float cm = __ldg(&cM[k1]);
-                const float s0 = a.scale / (1.f + a.taumu * (cm + c0));
-                const float sh = a.scale / (1.f + a.taumu * (cm + ch));
+                const float s0 = sym_scale(a.scale, a.taumu, cm, c0);
+                const float sh = sym_scale(a.scale, a.taumu, cm, ch);
                 const float pp = 0.5f * (s0 + sh), mm = 0.5f * (s0 - sh);
                 v[u] = make_float2(pp * C.x + mm * Cc.x, pp * C.y + mm * Cc.y);
             }
@@ -351,7 +364,7 @@ __global__ void __launch_bounds__(512, 1) k_cols_solve_p(float2* __restrict__ sp
             const float ck = __ldg(&cN[k2]);
 #pragma unroll
             for (int u = 0; u < E; u++) {
-                const float sc = a.scale / (1.f + a.taumu * (__ldg(&cM[t + u * T]) + ck));
+                const float sc = sym_scale(a.scale, a.taumu, __ldg(&cM[t + u * T]), ck);
                 v[u] = make_float2(v[u].x * sc, v[u].y * sc);
             }
         }

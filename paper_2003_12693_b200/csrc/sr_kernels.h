@@ -16,7 +16,7 @@ typedef void (*WbKernel)(const float*, const float*, float*, float*, const float
 
 RowKernel pick_row_fwd(int log2_h);       // fft_r2c.cu
 RowInvKernel pick_row_inv(int log2_h);    // fft_c2r.cu
-ColKernel pick_col(int log2_m);           // fft_cols.cu
+ColKernel pick_col(int log2_m, bool contig);   // fft_cols.cu; contig: whole image, G = 1
 typedef void (*ColPKernel)(float2*, const float2*, const float*, const float*, FftColArgs, int, int);
 ColPKernel pick_col_p(int log2_m);        // fft_cols.cu: persistent prefetching solve, M >= 4096
 // stencil_r<R>.cu; returns false if R is unsupported.  smem = dynamic shared bytes.

@@ -196,8 +196,7 @@ sr_status configure(sr_sb_ctx* c) {
     const int lgH = ilog2(H), lgM = ilog2(M);
     c->rfwd = pick_row_fwd(lgH);
     c->rinv = pick_row_inv(lgH);
-    c->cols = pick_col(lgM);
-    if (!c->rfwd || !c->rinv || !c->cols) return fail(c, SR_ERR_SHAPE, "no FFT kernel for this size");
+    if (!c->rfwd || !c->rinv || !pick_col(lgM, false)) return fail(c, SR_ERR_SHAPE, "no FFT kernel for this size");
     // Launch shapes (measured on B200, C3: smaller CTAs overlap load and FFT phases better):
     //  rows: rpc rows per CTA, 64..512 threads, <= ~72 KB shared;  E = min(16, H) values per thread
     const int E_h = H < 16 ? H : 16, T_h = H / E_h;
@@ -219,6 +218,7 @@ sr_status configure(sr_sb_ctx* c) {
         const int v = std::atoi(ev);
         if (v >= 1 && v <= H / P && (v & (v - 1)) == 0) G = v;
     }
+    c->cols = pick_col(lgM, !c->slab && G == 1);   // whole image, contiguous columns: immediate-offset access
     //  columns per CTA: >= 64 threads, <= 512 (a CTA may cover part of a column group)
     const int Hl = H / P;                            // spectrum columns this context solves
     const int E_m = M < 16 ? M : 16, T_m = M / E_m;
@@ -238,7 +238,10 @@ sr_status configure(sr_sb_ctx* c) {
     c->ra.M = Ml;
     c->ra.lg_rpc = ilog2(rpc);
     c->ra.lg_G = ilog2(G);
-    c->ra.SR = padded(H, G < 16 ? G : 1);
+    // Row stride of the shared rows: the transposed store/gather visits (rr, k2) with rr in [0, rpc) and
+    // G * rpc consecutive k2 per half-warp; SR = 16 / rpc (mod 16) makes rr * SR + k2 distinct mod 16,
+    // i.e. conflict-free 8-byte accesses (the former SR = G (mod 16) gave 2-way conflicts).
+    c->ra.SR = padded(H, rpc >= 16 ? 1 : (16 / rpc) & 15);
     c->ra.clip = 0.f;
     c->ra.accum = 0;
     c->rgrid = dim3(Ml / rpc, B, 1);

@@ -10,4 +10,12 @@ RowKernel pick_row_fwd(int lg) {
     }
     return nullptr;
 }
+// Launch-shape instances (log2 H, log2 rows per CTA, log2 G) of the measured configs: C1 128^2, C2 512^2,
+// C3 64 x 1024^2, C4 4096^2, C5 8192^2 (whole-image contexts; srsb.cu configure() picks these shapes).
+RowKernel pick_row_fwd_shape(int lg, int lg_rpc, int lg_G) {
+#define SRSB_SHAPE(LH, LR, LG_) if (lg == LH && lg_rpc == LR && lg_G == LG_) return k_rows_r2c<LH, 4, LR, LG_>;
+    SRSB_SHAPE(6, 4, 0) SRSB_SHAPE(8, 3, 0) SRSB_SHAPE(9, 3, 0) SRSB_SHAPE(11, 2, 1) SRSB_SHAPE(12, 1, 0)
+#undef SRSB_SHAPE
+    return pick_row_fwd(lg);
+}
 }  // namespace srsb

@@ -171,7 +171,7 @@ struct FftRowArgs {
 };
 
 // Row pass 1: F rows (N = 2H reals) -> transposed packed half spectrum.
-template <int LOGH, int LOGE>
+template <int LOGH, int LOGE, int LRPC = -1, int LG = -1>
 __global__ void __launch_bounds__(512) k_rows_r2c(const float* __restrict__ F, float2* __restrict__ spec,
                                                    const float2* __restrict__ twH,
                                                    const float2* __restrict__ twR, FftRowArgs a) {
@@ -179,7 +179,11 @@ __global__ void __launch_bounds__(512) k_rows_r2c(const float* __restrict__ F, f
     extern __shared__ float2 smem2[];
     const int tid = threadIdx.x;
     const int grp = tid / T, t = tid % T;
-    const int rpc = 1 << a.lg_rpc, G = 1 << a.lg_G;
+    // LRPC / LG >= 0: rows per CTA and column interleave fixed at compile time (the launch shapes of the
+    // measured configs), so the transposed addressing folds into immediate offsets
+    const int lg_rpc = LRPC >= 0 ? LRPC : a.lg_rpc, lg_G = LG >= 0 ? LG : a.lg_G;
+    const int rpc = 1 << lg_rpc, G = 1 << lg_G;
+    const int nthr = LRPC >= 0 ? (T << LRPC) : (int)blockDim.x;   // = blockDim.x
     const int b = blockIdx.y, m0 = blockIdx.x * rpc;
     float2* sm = smem2 + grp * a.SR;
     const float2* x = reinterpret_cast<const float2*>(F + b * a.plane + (long long)(m0 + grp) * (2 * H));
@@ -193,11 +197,11 @@ __global__ void __launch_bounds__(512) k_rows_r2c(const float* __restrict__ F, f
     float2* out = spec + (size_t)b * H * a.M;
 #pragma unroll
     for (int u = 0; u < E; u++) {
-        const int e = tid + u * blockDim.x;   // blockDim = rpc * T: exactly E elements per thread
+        const int e = tid + u * nthr;   // blockDim = rpc * T: exactly E elements per thread
         const int kk = e & (G - 1);
-        const int rr = (e >> a.lg_G) & (rpc - 1);
-        const int kg = e >> (a.lg_G + a.lg_rpc);
-        const int k2 = (kg << a.lg_G) + kk;
+        const int rr = (e >> lg_G) & (rpc - 1);
+        const int kg = e >> (lg_G + lg_rpc);
+        const int k2 = (kg << lg_G) + kk;
         const float2* row = smem2 + rr * a.SR;
         const float2 Zk = row[pad16(k2)];
         const float2 Zc = conjf2(row[pad16((H - k2) & (H - 1))]);
@@ -211,7 +215,7 @@ __global__ void __launch_bounds__(512) k_rows_r2c(const float* __restrict__ F, f
             const float2 wo = cmul(__ldg(&twR[k2]), O);
             X = make_float2(Ev.x + wo.x, Ev.y + wo.y);
         }
-        out[(((size_t)kg * a.M + m0 + rr) << a.lg_G) + kk] = X;
+        out[(((size_t)kg * a.M + m0 + rr) << lg_G) + kk] = X;
     }
 }
 
@@ -377,7 +381,7 @@ __global__ void __launch_bounds__(512, 1) k_cols_solve_p(float2* __restrict__ sp
 }
 
 // Row pass 2: transposed half spectrum -> inverse real FFT -> phi rows (accumulated, clamped).
-template <int LOGH, int LOGE>
+template <int LOGH, int LOGE, int LRPC = -1, int LG = -1>
 __global__ void __launch_bounds__(512) k_rows_c2r(const float2* __restrict__ spec, float* __restrict__ phi,
                                                    const float2* __restrict__ twH,
                                                    const float2* __restrict__ twR, FftRowArgs a) {
@@ -385,7 +389,11 @@ __global__ void __launch_bounds__(512) k_rows_c2r(const float2* __restrict__ spe
     extern __shared__ float2 smem2[];
     const int tid = threadIdx.x;
     const int grp = tid / T, t = tid % T;
-    const int rpc = 1 << a.lg_rpc, G = 1 << a.lg_G;
+    // LRPC / LG >= 0: rows per CTA and column interleave fixed at compile time (the launch shapes of the
+    // measured configs), so the transposed addressing folds into immediate offsets
+    const int lg_rpc = LRPC >= 0 ? LRPC : a.lg_rpc, lg_G = LG >= 0 ? LG : a.lg_G;
+    const int rpc = 1 << lg_rpc, G = 1 << lg_G;
+    const int nthr = LRPC >= 0 ? (T << LRPC) : (int)blockDim.x;   // = blockDim.x
     const int b = blockIdx.y, m0 = blockIdx.x * rpc;
     const float2* in = spec + (size_t)b * H * a.M;
     float2* out = reinterpret_cast<float2*>(phi + b * a.plane + (long long)(m0 + grp) * (2 * H));
@@ -402,12 +410,12 @@ __global__ void __launch_bounds__(512) k_rows_c2r(const float2* __restrict__ spe
         int sidx[E];
 #pragma unroll
         for (int u = 0; u < E; u++) {
-            const int e = tid + u * blockDim.x;
+            const int e = tid + u * nthr;
             const int kk = e & (G - 1);
-            const int rr = (e >> a.lg_G) & (rpc - 1);
-            const int kg = e >> (a.lg_G + a.lg_rpc);
-            const int k2 = (kg << a.lg_G) + kk;
-            tmp[u] = __ldcs(in + (((size_t)kg * a.M + m0 + rr) << a.lg_G) + kk);
+            const int rr = (e >> lg_G) & (rpc - 1);
+            const int kg = e >> (lg_G + lg_rpc);
+            const int k2 = (kg << lg_G) + kk;
+            tmp[u] = __ldcs(in + (((size_t)kg * a.M + m0 + rr) << lg_G) + kk);
             sidx[u] = rr * a.SR + pad16(k2);
         }
 #pragma unroll

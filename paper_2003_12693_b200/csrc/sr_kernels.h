@@ -16,6 +16,8 @@ typedef void (*WbKernel)(const float*, const float*, float*, float*, const float
 
 RowKernel pick_row_fwd(int log2_h);       // fft_r2c.cu
 RowInvKernel pick_row_inv(int log2_h);    // fft_c2r.cu
+RowKernel pick_row_fwd_shape(int log2_h, int lg_rpc, int lg_G);      // specialised launch shapes, else generic
+RowInvKernel pick_row_inv_shape(int log2_h, int lg_rpc, int lg_G);
 ColKernel pick_col(int log2_m, bool contig);   // fft_cols.cu; contig: whole image, G = 1
 typedef void (*ColPKernel)(float2*, const float2*, const float*, const float*, FftColArgs, int, int);
 ColPKernel pick_col_p(int log2_m);        // fft_cols.cu: persistent prefetching solve, M >= 4096

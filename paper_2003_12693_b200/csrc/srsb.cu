@@ -218,7 +218,9 @@ sr_status configure(sr_sb_ctx* c) {
         const int v = std::atoi(ev);
         if (v >= 1 && v <= H / P && (v & (v - 1)) == 0) G = v;
     }
-    c->cols = pick_col(lgM, !c->slab && G == 1);   // whole image, contiguous columns: immediate-offset access
+    c->cols = pick_col(lgM, !c->slab && G == 1);
+    c->rfwd = pick_row_fwd_shape(lgH, ilog2(rpc), ilog2(G));
+    c->rinv = pick_row_inv_shape(lgH, ilog2(rpc), ilog2(G));   // whole image, contiguous columns: immediate-offset access
     //  columns per CTA: >= 64 threads, <= 512 (a CTA may cover part of a column group)
     const int Hl = H / P;                            // spectrum columns this context solves
     const int E_m = M < 16 ? M : 16, T_m = M / E_m;

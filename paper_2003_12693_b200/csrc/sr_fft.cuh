@@ -380,9 +380,18 @@ __global__ void __launch_bounds__(512, 1) k_cols_solve_p(float2* __restrict__ sp
     }
 }
 
+#define H_OF(L) (1 << (L))
 // Row pass 2: transposed half spectrum -> inverse real FFT -> phi rows (accumulated, clamped).
+#ifndef SRSB_C2R_MINB
+#define SRSB_C2R_MINB 1     // resident CTAs per SM asked of ptxas for the <= 256-thread launch-shape instances
+#endif
+#ifndef SRSB_C2R_LATE_OLD
+#define SRSB_C2R_LATE_OLD 0 // 1: fetch the accumulation source after the FFT (fewer live registers)
+#endif
 template <int LOGH, int LOGE, int LRPC = -1, int LG = -1>
-__global__ void __launch_bounds__(512) k_rows_c2r(const float2* __restrict__ spec, float* __restrict__ phi,
+__global__ void __launch_bounds__(LRPC >= 0 ? ((H_OF(LOGH) / (1 << LOGE)) << (LRPC >= 0 ? LRPC : 0)) : 512,
+                                  (LRPC >= 0 && ((H_OF(LOGH) / (1 << LOGE)) << (LRPC >= 0 ? LRPC : 0)) <= 256) ? SRSB_C2R_MINB : 1)
+k_rows_c2r(const float2* __restrict__ spec, float* __restrict__ phi,
                                                    const float2* __restrict__ twH,
                                                    const float2* __restrict__ twR, FftRowArgs a) {
     constexpr int H = 1 << LOGH, E = 1 << LOGE, T = H / E;
@@ -399,7 +408,7 @@ __global__ void __launch_bounds__(512) k_rows_c2r(const float2* __restrict__ spe
     float2* out = reinterpret_cast<float2*>(phi + b * a.plane + (long long)(m0 + grp) * (2 * H));
     // accumulation source (phi of the previous sweep), fetched first: its latency hides behind the FFT
     float2 old[E];
-    if (a.accum) {
+    if (!SRSB_C2R_LATE_OLD && a.accum) {
 #pragma unroll
         for (int u = 0; u < E; u++) old[u] = out[t + u * T];
     }
@@ -441,6 +450,10 @@ __global__ void __launch_bounds__(512) k_rows_c2r(const float2* __restrict__ spe
     }
     __syncthreads();
     fft_stages<LOGH, LOGE, 0, true>(v, sm, t, twH);
+    if (SRSB_C2R_LATE_OLD && a.accum) {
+#pragma unroll
+        for (int u = 0; u < E; u++) old[u] = out[t + u * T];
+    }
     float dsum = 0.f, osum = 0.f;
 #pragma unroll
     for (int u = 0; u < E; u++) {

@@ -764,6 +764,34 @@ __device__ __forceinline__ void rhs_points_tma(const float* Ps, const float* W1s
     }
 }
 
+// L2 prefetch in the TMA stencils (k_rhs_tma: SRSB_RHS_PF, k_wb_tma: SRSB_WB_PF):
+//   bit 0: the CTA's own group 2 at its start (its later TMA load then hits L2);
+//   bit 1: both groups of the CTA SRSB_*_PF_DIST launches ahead (scheduled later on a freed slot).
+// Measured on C3 (whole step, 2 steps each): none 21.05k, rhs bit 1 + wb bit 1 21.36k, rhs 2 + wb 1 21.24k /
+// 21.20k Mpx-iter/s (rhs 0.447 -> 0.422 ms, wb 0.519 -> 0.488 ms in isolation; under the sustained step the
+// extra traffic meets the power cap, so the step gains ~1 %); rhs 2 at distance 888: 20.27k.
+#ifndef SRSB_RHS_PF
+#define SRSB_RHS_PF 2
+#endif
+#ifndef SRSB_WB_PF
+#define SRSB_WB_PF 1
+#endif
+#ifndef SRSB_RHS_PF_DIST
+#define SRSB_RHS_PF_DIST 444 // 148 SMs x 3 resident CTAs
+#endif
+#ifndef SRSB_WB_PF_DIST
+#define SRSB_WB_PF_DIST 444
+#endif
+// tile coordinates of the CTA `ahead` launches after this one (blockIdx.x fastest); false past the grid
+__device__ __forceinline__ bool tile_ahead(int ahead, int& bx, int& by, int& bz) {
+    const long long lin = blockIdx.x + (long long)gridDim.x * (blockIdx.y + (long long)gridDim.y * blockIdx.z) + ahead;
+    if (lin >= (long long)gridDim.x * gridDim.y * gridDim.z) return false;
+    bx = (int)(lin % gridDim.x);
+    by = (int)((lin / gridDim.x) % gridDim.y);
+    bz = (int)(lin / ((long long)gridDim.x * gridDim.y));
+    return true;
+}
+
 template <int R, int SHAPE, bool LEQ>
 __global__ void __launch_bounds__(256, 3) k_rhs_tma(const __grid_constant__ RhsMaps maps,
                                                     const float* __restrict__ phi, float* __restrict__ D,
@@ -792,6 +820,21 @@ __global__ void __launch_bounds__(256, 3) k_rhs_tma(const __grid_constant__ RhsM
         tma_load_3d(Ps, &maps.phi, &bar[0], col0 - G::CA, ar - G::HR, img);
         tma_load_3d(W1s, &maps.w, &bar[0], col0 - G::CA, ar - G::HR, 2 * img);
         tma_load_3d(W2s, &maps.w, &bar[0], col0 - G::CA, ar - G::HR, 2 * img + 1);
+        if (SRSB_RHS_PF & 1) {
+            tma_prefetch_3d(&maps.b, col0 - 4, ar - 1, 2 * img);
+            tma_prefetch_3d(&maps.b, col0 - 4, ar - 1, 2 * img + 1);
+            tma_prefetch_3d(&maps.g, col0, ar, img);
+        }
+        int bx, by, bz;
+        if ((SRSB_RHS_PF & 2) && tile_ahead(SRSB_RHS_PF_DIST, bx, by, bz)) {
+            const int c = bx * G::TW, r = a.gh + by * G::TH;
+            tma_prefetch_3d(&maps.phi, c - G::CA, r - G::HR, bz);
+            tma_prefetch_3d(&maps.w, c - G::CA, r - G::HR, 2 * bz);
+            tma_prefetch_3d(&maps.w, c - G::CA, r - G::HR, 2 * bz + 1);
+            tma_prefetch_3d(&maps.b, c - 4, r - 1, 2 * bz);
+            tma_prefetch_3d(&maps.b, c - 4, r - 1, 2 * bz + 1);
+            tma_prefetch_3d(&maps.g, c, r, bz);
+        }
     }
     mbar_wait(&bar[0], 0);
     // u = h(phi) w over the tile + R halo, as 16-byte chunks (2 px x 2 channels) in TileGeom's layout
@@ -866,6 +909,21 @@ __global__ void __launch_bounds__(256, 3) k_wb_tma(const __grid_constant__ RhsMa
         tma_load_3d(Ps, &maps.phi, &bar[0], col0 - G::CA, ar - G::HR, img);
         tma_load_3d(W1s, &maps.w, &bar[0], col0 - G::CA, ar - G::HR, 2 * img);
         tma_load_3d(W2s, &maps.w, &bar[0], col0 - G::CA, ar - G::HR, 2 * img + 1);
+        if (SRSB_WB_PF & 1) {
+            tma_prefetch_3d(&maps.bt, col0, ar, 2 * img);
+            tma_prefetch_3d(&maps.bt, col0, ar, 2 * img + 1);
+            tma_prefetch_3d(&maps.g, col0, ar, img);
+        }
+        int bx, by, bz;
+        if ((SRSB_WB_PF & 2) && tile_ahead(SRSB_WB_PF_DIST, bx, by, bz)) {
+            const int c = bx * G::TW, r = a.gh + by * G::TH;
+            tma_prefetch_3d(&maps.phi, c - G::CA, r - G::HR, bz);
+            tma_prefetch_3d(&maps.w, c - G::CA, r - G::HR, 2 * bz);
+            tma_prefetch_3d(&maps.w, c - G::CA, r - G::HR, 2 * bz + 1);
+            tma_prefetch_3d(&maps.bt, c, r, 2 * bz);
+            tma_prefetch_3d(&maps.bt, c, r, 2 * bz + 1);
+            tma_prefetch_3d(&maps.g, c, r, bz);
+        }
     }
     mbar_wait(&bar[0], 0);
     stage_u_tma<R, LEQ, G>(U, Ps, W1s, W2s, row0, tid, a);

@@ -195,27 +195,38 @@ __global__ void __launch_bounds__(512) k_rows_r2c(const float* __restrict__ F, f
     for (int u = 0; u < E; u++) sm[pad16(t + u * T)] = v[u];
     __syncthreads();
     float2* out = spec + (size_t)b * H * a.M;
-#pragma unroll
-    for (int u = 0; u < E; u++) {
-        const int e = tid + u * nthr;   // blockDim = rpc * T: exactly E elements per thread
-        const int kk = e & (G - 1);
-        const int rr = (e >> lg_G) & (rpc - 1);
-        const int kg = e >> (lg_G + lg_rpc);
-        const int k2 = (kg << lg_G) + kk;
+    // real-FFT split of bin k2 of shared row rr
+    auto split = [&](int rr, int k2) -> float2 {
         const float2* row = smem2 + rr * a.SR;
         const float2 Zk = row[pad16(k2)];
         const float2 Zc = conjf2(row[pad16((H - k2) & (H - 1))]);
-        float2 X;
-        if (k2 == 0) {
-            X = make_float2(Zk.x + Zk.y, Zk.x - Zk.y);  // (X[0], X[N/2]) packed
-        } else {
-            const float2 Ev = make_float2(0.5f * (Zk.x + Zc.x), 0.5f * (Zk.y + Zc.y));
-            const float2 D = make_float2(0.5f * (Zk.x - Zc.x), 0.5f * (Zk.y - Zc.y));
-            const float2 O = make_float2(D.y, -D.x);  // -i D
-            const float2 wo = cmul(__ldg(&twR[k2]), O);
-            X = make_float2(Ev.x + wo.x, Ev.y + wo.y);
+        if (k2 == 0) return make_float2(Zk.x + Zk.y, Zk.x - Zk.y);  // (X[0], X[N/2]) packed
+        const float2 Ev = make_float2(0.5f * (Zk.x + Zc.x), 0.5f * (Zk.y + Zc.y));
+        const float2 D = make_float2(0.5f * (Zk.x - Zc.x), 0.5f * (Zk.y - Zc.y));
+        const float2 O = make_float2(D.y, -D.x);  // -i D
+        const float2 wo = cmul(__ldg(&twR[k2]), O);
+        return make_float2(Ev.x + wo.x, Ev.y + wo.y);
+    };
+    if constexpr (LG == 0 && LRPC >= 1) {
+        // contiguous columns: rows 2 rp, 2 rp + 1 of bin k2 are adjacent -> one 16-byte store per pair
+        constexpr int LRP = LRPC - 1;
+#pragma unroll
+        for (int u = 0; u < E / 2; u++) {
+            const int e = tid + u * nthr;
+            const int rp = e & ((1 << LRP) - 1), k2 = e >> LRP;
+            const float2 X0 = split(2 * rp, k2), X1 = split(2 * rp + 1, k2);
+            *reinterpret_cast<float4*>(out + (size_t)k2 * a.M + m0 + 2 * rp) = make_float4(X0.x, X0.y, X1.x, X1.y);
         }
-        out[(((size_t)kg * a.M + m0 + rr) << lg_G) + kk] = X;
+    } else {
+#pragma unroll
+        for (int u = 0; u < E; u++) {
+            const int e = tid + u * nthr;   // blockDim = rpc * T: exactly E elements per thread
+            const int kk = e & (G - 1);
+            const int rr = (e >> lg_G) & (rpc - 1);
+            const int kg = e >> (lg_G + lg_rpc);
+            const int k2 = (kg << lg_G) + kk;
+            out[(((size_t)kg * a.M + m0 + rr) << lg_G) + kk] = split(rr, k2);
+        }
     }
 }
 
@@ -414,7 +425,24 @@ k_rows_c2r(const float2* __restrict__ spec, float* __restrict__ phi,
     }
     // transposed gather: blockDim = rpc * T threads, rpc * H elements -> exactly E per thread;
     // all E loads are issued before the shared stores
-    {
+    if constexpr (LG == 0 && LRPC >= 1) {
+        // contiguous columns: rows 2 rp, 2 rp + 1 of bin k2 are adjacent -> one 16-byte load per pair
+        constexpr int LRP = LRPC - 1;
+        float4 tmp[E / 2];
+        int sidx[E / 2];
+#pragma unroll
+        for (int u = 0; u < E / 2; u++) {
+            const int e = tid + u * nthr;
+            const int rp = e & ((1 << LRP) - 1), k2 = e >> LRP;
+            tmp[u] = __ldcs(reinterpret_cast<const float4*>(in + (size_t)k2 * a.M + m0 + 2 * rp));
+            sidx[u] = 2 * rp * a.SR + pad16(k2);
+        }
+#pragma unroll
+        for (int u = 0; u < E / 2; u++) {
+            smem2[sidx[u]] = make_float2(tmp[u].x, tmp[u].y);
+            smem2[sidx[u] + a.SR] = make_float2(tmp[u].z, tmp[u].w);
+        }
+    } else {
         float2 tmp[E];
         int sidx[E];
 #pragma unroll

@@ -396,12 +396,16 @@ __global__ void __launch_bounds__(512, 1) k_cols_solve_p(float2* __restrict__ sp
 #ifndef SRSB_C2R_MINB
 #define SRSB_C2R_MINB 1     // resident CTAs per SM asked of ptxas for the <= 256-thread launch-shape instances
 #endif
+#ifndef SRSB_C2R_MINB_BIG
+#define SRSB_C2R_MINB_BIG 1 // the same for the 512-thread instances (H = 4096: C5)
+#endif
 #ifndef SRSB_C2R_LATE_OLD
 #define SRSB_C2R_LATE_OLD 0 // 1: fetch the accumulation source after the FFT (fewer live registers)
 #endif
 template <int LOGH, int LOGE, int LRPC = -1, int LG = -1>
 __global__ void __launch_bounds__(LRPC >= 0 ? ((H_OF(LOGH) / (1 << LOGE)) << (LRPC >= 0 ? LRPC : 0)) : 512,
-                                  (LRPC >= 0 && ((H_OF(LOGH) / (1 << LOGE)) << (LRPC >= 0 ? LRPC : 0)) <= 256) ? SRSB_C2R_MINB : 1)
+                                  (LRPC >= 0 && ((H_OF(LOGH) / (1 << LOGE)) << (LRPC >= 0 ? LRPC : 0)) <= 256) ? SRSB_C2R_MINB
+                                  : (LRPC >= 0 ? SRSB_C2R_MINB_BIG : 1))
 k_rows_c2r(const float2* __restrict__ spec, float* __restrict__ phi,
                                                    const float2* __restrict__ twH,
                                                    const float2* __restrict__ twR, FftRowArgs a) {

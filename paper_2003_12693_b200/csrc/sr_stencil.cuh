@@ -678,11 +678,27 @@ struct TmaGeom {
 
 // u = h(phi) w over the tile + R halo from the group-1 boxes, as 16-byte chunks (2 px x 2 channels)
 // in TileGeom's layout; rows outside the image give u = 0 (reading Q5).  Branch-free, f32x2.
+#ifndef SRSB_STAGE_U_OLD
+#define SRSB_STAGE_U_OLD 0   // 1: the strided loop with a division per chunk (A/B reference)
+#endif
 template <int R, bool LEQ, class G>
 __device__ __forceinline__ void stage_u_tma(float4* __restrict__ U, const float* Ps, const float* W1s,
                                             const float* W2s, int row0, int tid, const StencilArgs& a) {
+#if SRSB_STAGE_U_OLD
     for (int k = tid; k < G::UROWS * G::UCH; k += 256) {
         const int r = k / G::UCH, f = k - r * G::UCH;
+#else
+    // fixed trip count, (r, f) stepped incrementally (256 = DR rows + DF chunks)
+    constexpr int TOT = G::UROWS * G::UCH, NIT = (TOT + 255) / 256, DR = 256 / G::UCH, DF = 256 % G::UCH;
+    int r = tid / G::UCH, f = tid - (tid / G::UCH) * G::UCH;
+#pragma unroll
+    for (int it = 0; it < NIT; it++, r += DR, f += DF) {
+        if (f >= G::UCH) {
+            f -= G::UCH;
+            r++;
+        }
+        if (it == NIT - 1 && tid + it * 256 >= TOT) break;
+#endif
         const int gr = row0 - R + r + a.row_off;   // global row
         const int o = (r + G::HR - R) * G::PW + (G::CA - G::RA) + 2 * f;
         const float2 P = *reinterpret_cast<const float2*>(Ps + o);

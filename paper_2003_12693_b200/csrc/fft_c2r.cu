@@ -14,7 +14,7 @@ RowInvKernel pick_row_inv(int lg) {
 // C3 64 x 1024^2, C4 4096^2, C5 8192^2 (whole-image contexts; srsb.cu configure() picks these shapes).
 RowInvKernel pick_row_inv_shape(int lg, int lg_rpc, int lg_G) {
 #define SRSB_SHAPE(LH, LR, LG_) if (lg == LH && lg_rpc == LR && lg_G == LG_) return k_rows_c2r<LH, 4, LR, LG_>;
-    SRSB_SHAPE(6, 4, 0) SRSB_SHAPE(8, 3, 0) SRSB_SHAPE(9, 3, 0) SRSB_SHAPE(11, 2, 0) SRSB_SHAPE(11, 2, 1) SRSB_SHAPE(12, 1, 0)
+    SRSB_SHAPE(6, 4, 0) SRSB_SHAPE(8, 3, 0) SRSB_SHAPE(9, 1, 0) SRSB_SHAPE(9, 2, 0) SRSB_SHAPE(9, 3, 0) SRSB_SHAPE(9, 4, 0) SRSB_SHAPE(11, 2, 0) SRSB_SHAPE(11, 2, 1) SRSB_SHAPE(12, 1, 0)
 #undef SRSB_SHAPE
     return pick_row_inv(lg);
 }

@@ -93,6 +93,9 @@ struct sr_sb_ctx {
     StencilArgs sa{};
     dim3 rgrid, rblock, cgrid, cblock, sgrid, sblock;
     int rsmem = 0, csmem = 0, ssmem = 0;
+    FftRowArgs ra_inv{};            // c2r launch shape (may use fewer rows per CTA than r2c when G = 1)
+    dim3 rgrid_inv, rblock_inv;
+    int rsmem_inv = 0;
     // NEXT-1 monitor: per image [E_g, E_a, E_r, E_pen, (|dphi_s|^2, |phi_s|^2) x S]
     double* stats = nullptr;
     int stats_stride = 0;
@@ -218,9 +221,8 @@ sr_status configure(sr_sb_ctx* c) {
         const int v = std::atoi(ev);
         if (v >= 1 && v <= H / P && (v & (v - 1)) == 0) G = v;
     }
-    c->cols = pick_col(lgM, !c->slab && G == 1);
+    c->cols = pick_col(lgM, !c->slab && G == 1);   // whole image, contiguous columns: immediate-offset access
     c->rfwd = pick_row_fwd_shape(lgH, ilog2(rpc), ilog2(G));
-    c->rinv = pick_row_inv_shape(lgH, ilog2(rpc), ilog2(G));   // whole image, contiguous columns: immediate-offset access
     //  columns per CTA: >= 64 threads, <= 512 (a CTA may cover part of a column group)
     const int Hl = H / P;                            // spectrum columns this context solves
     const int E_m = M < 16 ? M : 16, T_m = M / E_m;
@@ -249,6 +251,22 @@ sr_status configure(sr_sb_ctx* c) {
     c->rgrid = dim3(Ml / rpc, B, 1);
     c->rblock = dim3(rpc * T_h, 1, 1);
     c->rsmem = rpc * c->ra.SR * (int)sizeof(float2);
+    {   // c2r: with contiguous columns (G = 1, whole image) the spectrum layout does not depend on the rows
+        // per CTA, so the inverse pass may take its own (SRSB_RPC_INV, tuning knob)
+        int ri = rpc;
+        const char* ev = std::getenv("SRSB_RPC_INV");
+        if (ev && G == 1 && !c->slab) {
+            const int v = std::atoi(ev);
+            if (v >= 2 && v <= Ml && v * T_h <= 512 && (v & (v - 1)) == 0) ri = v;
+        }
+        c->ra_inv = c->ra;
+        c->ra_inv.lg_rpc = ilog2(ri);
+        c->ra_inv.SR = padded(H, ri >= 16 ? 1 : (16 / ri) & 15);
+        c->rgrid_inv = dim3(Ml / ri, B, 1);
+        c->rblock_inv = dim3(ri * T_h, 1, 1);
+        c->rsmem_inv = ri * c->ra_inv.SR * (int)sizeof(float2);
+        c->rinv = pick_row_inv_shape(lgH, ilog2(ri), ilog2(G));
+    }
     c->ca.H = H;
     c->ca.lg_G = ilog2(G);
     c->ca.lg_cpc = ilog2(cpc);
@@ -337,7 +355,7 @@ sr_status configure(sr_sb_ctx* c) {
     }
     // opt-in shared memory above 48 KB
     CK(cudaFuncSetAttribute((const void*)c->rfwd, cudaFuncAttributeMaxDynamicSharedMemorySize, c->rsmem));
-    CK(cudaFuncSetAttribute((const void*)c->rinv, cudaFuncAttributeMaxDynamicSharedMemorySize, c->rsmem));
+    CK(cudaFuncSetAttribute((const void*)c->rinv, cudaFuncAttributeMaxDynamicSharedMemorySize, c->rsmem_inv));
     CK(cudaFuncSetAttribute((const void*)c->cols, cudaFuncAttributeMaxDynamicSharedMemorySize, c->csmem));
     if (c->cols_p) {
         c->cp_threads = M / 16;
@@ -437,13 +455,13 @@ void enq_cols(sr_sb_ctx* c) {
     prof_end(c, SR_K_COLS_SOLVE);
 }
 void enq_c2r(sr_sb_ctx* c, float* out, float clip, int accum, int sweep = -1) {
-    FftRowArgs ra = c->ra;
+    FftRowArgs ra = c->ra_inv;
     ra.accum = accum;
     ra.clip = clip;
     ra.stats = (c->stats && sweep >= 0) ? c->stats + 4 + 2 * sweep : nullptr;
     ra.stats_stride = c->stats_stride;
     prof_begin(c);
-    c->rinv<<<c->rgrid, c->rblock, c->rsmem, c->s>>>(c->spec, out, c->twH, c->twR, ra);
+    c->rinv<<<c->rgrid_inv, c->rblock_inv, c->rsmem_inv, c->s>>>(c->spec, out, c->twH, c->twR, ra);
     prof_end(c, SR_K_ROWS_C2R);
 }
 void enq_rhs(sr_sb_ctx* c, float* F) {

@@ -31,6 +31,30 @@ namespace srsb {
 #define SRSB_COLS_MAXNREG_BIG 64   // M >= 4096: 256 / 512-thread column CTAs, 2 resident per SM instead of 1
 #endif
 
+// L2 prefetch of the input of the CTA launched SRSB_*_PF_DIST CTAs later (about one full wave of
+// resident CTAs ahead), issued by thread 0 at the start: bit 0 r2c (its 8 rows of D), bit 1 the
+// contiguous-column solve (its column), bit 2 c2r (its rows of psi).  0 = off.
+#ifndef SRSB_FFT_PF
+#define SRSB_FFT_PF 0
+#endif
+#ifndef SRSB_R2C_PF_DIST
+#define SRSB_R2C_PF_DIST 592    // 148 SMs x 4 resident CTAs
+#endif
+#ifndef SRSB_COLS_PF_DIST
+#define SRSB_COLS_PF_DIST 1480  // 148 x 10
+#endif
+#ifndef SRSB_C2R_PF_DIST
+#define SRSB_C2R_PF_DIST 296    // 148 x 2
+#endif
+// 2-D grid block `ahead` launches after this one (blockIdx.x fastest); false past the grid
+__device__ __forceinline__ bool block_ahead_2d(int ahead, int& bx, int& by) {
+    const int lin = blockIdx.x + gridDim.x * blockIdx.y + ahead;
+    if (lin >= (int)(gridDim.x * gridDim.y)) return false;
+    bx = lin % gridDim.x;
+    by = lin / gridDim.x;
+    return true;
+}
+
 // float2 shared-memory index with one pad slot per 16 complex values (128 B): strided butterfly
 // accesses with power-of-two strides <= 16 hit 16 distinct 8-byte bank pairs per half-warp.
 __device__ __forceinline__ int pad16(int i) { return i + (i >> 4); }
@@ -186,6 +210,11 @@ __global__ void __launch_bounds__(512) k_rows_r2c(const float* __restrict__ F, f
     const int nthr = LRPC >= 0 ? (T << LRPC) : (int)blockDim.x;   // = blockDim.x
     const int b = blockIdx.y, m0 = blockIdx.x * rpc;
     float2* sm = smem2 + grp * a.SR;
+    if ((SRSB_FFT_PF & 1) && tid == 0) {
+        int bx, by;
+        if (block_ahead_2d(SRSB_R2C_PF_DIST, bx, by))
+            bulk_prefetch_l2(F + by * a.plane + (long long)(bx * rpc) * (2 * H), (uint32_t)(rpc * 2 * H * 4));
+    }
     const float2* x = reinterpret_cast<const float2*>(F + b * a.plane + (long long)(m0 + grp) * (2 * H));
     float2 v[E];
 #pragma unroll
@@ -273,6 +302,12 @@ __global__ void __maxnreg__(LOGM >= 12 ? SRSB_COLS_MAXNREG_BIG : SRSB_COLS_MAXNR
         return s * a.seg_stride + ((long long)((kg << a.lg_seg) + mr) << a.lg_G);
     };
     float2* col = spec + b * a.bstride + ((long long)k2l << LOGM);   // CONTIG only
+    if (CONTIG && (SRSB_FFT_PF & 2) && tid == 0) {
+        int bx, by;
+        if (block_ahead_2d(SRSB_COLS_PF_DIST, bx, by))
+            bulk_prefetch_l2(spec + by * a.bstride + ((long long)(bx << a.lg_cpc) << LOGM),
+                             (uint32_t)((M << a.lg_cpc) * sizeof(float2)));
+    }
     float2 v[E];
 #pragma unroll
     for (int u = 0; u < E; u++) v[u] = CONTIG ? col[t + u * T] : base[addr(t + u * T)];
@@ -421,6 +456,11 @@ k_rows_c2r(const float2* __restrict__ spec, float* __restrict__ phi,
     const int b = blockIdx.y, m0 = blockIdx.x * rpc;
     const float2* in = spec + (size_t)b * H * a.M;
     float2* out = reinterpret_cast<float2*>(phi + b * a.plane + (long long)(m0 + grp) * (2 * H));
+    if ((SRSB_FFT_PF & 4) && a.accum && tid == 0) {
+        int bx, by;
+        if (block_ahead_2d(SRSB_C2R_PF_DIST, bx, by))
+            bulk_prefetch_l2(phi + by * a.plane + (long long)(bx * rpc) * (2 * H), (uint32_t)(rpc * 2 * H * 4));
+    }
     // accumulation source (phi of the previous sweep), fetched first: its latency hides behind the FFT
     float2 old[E];
     if (!SRSB_C2R_LATE_OLD && a.accum) {

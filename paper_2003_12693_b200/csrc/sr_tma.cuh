@@ -49,6 +49,11 @@ __device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, 
                  : "memory");
 }
 
+// L2 prefetch of contiguous bytes (multiple of 16, 16-byte aligned); no completion mechanism
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // contiguous bytes (multiple of 16, 16-byte aligned) global -> shared, completing on bar
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(

@@ -649,7 +649,13 @@ struct RhsMaps {
     CUtensorMap bt;             // b, box TW x TH (the w/b update reads b at the tile only)
 };
 
-constexpr int TMA_TH = 32;                                            // tile rows of the TMA kernels
+#ifndef SRSB_TMA_TH
+#define SRSB_TMA_TH 32      // tile rows of the TMA kernels (a multiple of 8: 8 thread rows x TH/8 rows)
+#endif
+#ifndef SRSB_TMA_MINB
+#define SRSB_TMA_MINB 3     // resident CTAs per SM asked of ptxas (shared memory allows 3 at TH = 32)
+#endif
+constexpr int TMA_TH = SRSB_TMA_TH;
 constexpr int tma_hr(int R) { return R > 1 ? R : 1; }                 // box row halo (the Laplacian needs 1)
 // box column halo: >= the u halo RA and >= 1 (Laplacian), rounded to 4 columns so every box row is a
 // multiple of 32 bytes (box rows of 272 / 304 bytes faulted with an illegal instruction on B200)
@@ -660,7 +666,7 @@ constexpr int TMA_BW = ST_TW + 8, TMA_BH = TMA_TH + 1;                 // b box:
 
 template <int R>
 struct TmaGeom {
-    static constexpr int TH = TMA_TH, TW = ST_TW, RT = 4;   // 8 thread rows x 4 rows, 32 x 2 columns
+    static constexpr int TH = TMA_TH, TW = ST_TW, RT = TMA_TH / 8;   // 8 thread rows x RT rows, 32 x 2 columns
     static constexpr int RA = TileGeom<R>::RA;           // u halo columns (even)
     static constexpr int HR = tma_hr(R), CA = tma_ca(R);
     static constexpr int PW = tma_pw(R), PH = tma_ph(R);
@@ -793,10 +799,10 @@ __device__ __forceinline__ void rhs_points_tma(const float* Ps, const float* W1s
 #define SRSB_WB_PF 1
 #endif
 #ifndef SRSB_RHS_PF_DIST
-#define SRSB_RHS_PF_DIST 444 // 148 SMs x 3 resident CTAs
+#define SRSB_RHS_PF_DIST (148 * SRSB_TMA_MINB) // one wave of resident CTAs
 #endif
 #ifndef SRSB_WB_PF_DIST
-#define SRSB_WB_PF_DIST 444
+#define SRSB_WB_PF_DIST (148 * SRSB_TMA_MINB)
 #endif
 // tile coordinates of the CTA `ahead` launches after this one (blockIdx.x fastest); false past the grid
 __device__ __forceinline__ bool tile_ahead(int ahead, int& bx, int& by, int& bz) {
@@ -809,7 +815,7 @@ __device__ __forceinline__ bool tile_ahead(int ahead, int& bx, int& by, int& bz)
 }
 
 template <int R, int SHAPE, bool LEQ>
-__global__ void __launch_bounds__(256, 3) k_rhs_tma(const __grid_constant__ RhsMaps maps,
+__global__ void __launch_bounds__(256, SRSB_TMA_MINB) k_rhs_tma(const __grid_constant__ RhsMaps maps,
                                                     const float* __restrict__ phi, float* __restrict__ D,
                                                     StencilArgs a) {
     using G = TmaGeom<R>;
@@ -899,7 +905,7 @@ struct WbGeom {
 };
 
 template <int R, int SHAPE, int MODE, bool UPDATE_B, bool LEQ, bool MON = false>
-__global__ void __launch_bounds__(256, 3) k_wb_tma(const __grid_constant__ RhsMaps maps, float* __restrict__ w_out,
+__global__ void __launch_bounds__(256, SRSB_TMA_MINB) k_wb_tma(const __grid_constant__ RhsMaps maps, float* __restrict__ w_out,
                                                    float* __restrict__ bv, int* __restrict__ flag, StencilArgs a) {
     using G = WbGeom<R>;
     extern __shared__ unsigned char sm_raw[];

@@ -351,3 +351,22 @@ def test_degenerate_cases(S, orc):
             phi = _np(sv.get_phi())
         ref = orc.run(q, img[0], phi0[0], 5)["phi"]
         assert np.max(np.abs(phi[0] - ref)) <= 1e-4, over
+
+
+@pytest.mark.parametrize("M,N,env", [(1024, 1024, {"SRSB_RPC": "4"}), (1024, 1024, {"SRSB_G": "2"}),
+                                     (512, 512, {"SRSB_RPC": "2"}), (128, 128, {"SRSB_G": "2"}),
+                                     (1024, 1024, {"SRSB_RPC_INV": "4"})])
+def test_launch_shape_instances_bitwise(S, M, N, env, monkeypatch):
+    """The launch-shape instances of the row passes (rows per CTA / interleave as template constants,
+    paired 16-byte transposed accesses) and the contiguous-column solve give bitwise the same Eq. (33)
+    solve as the generic kernels: other shapes / layouts are forced with the tuning knobs (read at
+    context creation), the butterflies and per-element arithmetic are identical."""
+    p = _params(4)
+    F = np.random.default_rng(7).standard_normal((2, M, N)).astype(np.float32)
+    with _solver(S, M, N, 2, p) as sv:
+        ref = _np(sv.debug_solve(_cuda(F)))
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    with _solver(S, M, N, 2, p) as sv:
+        out = _np(sv.debug_solve(_cuda(F)))
+    assert np.array_equal(out, ref)

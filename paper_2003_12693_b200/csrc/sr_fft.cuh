@@ -37,6 +37,9 @@ namespace srsb {
 #ifndef SRSB_FFT_PF
 #define SRSB_FFT_PF 0
 #endif
+#ifndef SRSB_R2C_MIRROR
+#define SRSB_R2C_MIRROR 1   // r2c split: bins k and H - k from one pair of shared reads (0: one bin per pair)
+#endif
 #ifndef SRSB_R2C_PF_DIST
 #define SRSB_R2C_PF_DIST 592    // 148 SMs x 4 resident CTAs
 #endif
@@ -236,7 +239,48 @@ __global__ void __launch_bounds__(512) k_rows_r2c(const float* __restrict__ F, f
         const float2 wo = cmul(__ldg(&twR[k2]), O);
         return make_float2(Ev.x + wo.x, Ev.y + wo.y);
     };
-    if constexpr (LG == 0 && LRPC >= 1) {
+    if constexpr (LG == 0 && LRPC >= 1 && E >= 4 && SRSB_R2C_MIRROR) {
+        // contiguous columns, bins k2 and H - k2 from the same two shared reads per row (the split of
+        // one is the split of the other with the operands swapped); rows 2 rp, 2 rp + 1 of a bin are
+        // adjacent -> 16-byte stores.  k2 = 0 also emits the self-mirrored bin H / 2.
+        constexpr int LRP = LRPC - 1;
+        auto split2 = [&](float2 Za, float2 Zb, float2 tw) -> float2 {   // Zb = Z[H - k]
+            const float2 Zc = conjf2(Zb);
+            const float2 Ev = make_float2(0.5f * (Za.x + Zc.x), 0.5f * (Za.y + Zc.y));
+            const float2 D = make_float2(0.5f * (Za.x - Zc.x), 0.5f * (Za.y - Zc.y));
+            const float2 O = make_float2(D.y, -D.x);  // -i D
+            const float2 wo = cmul(tw, O);
+            return make_float2(Ev.x + wo.x, Ev.y + wo.y);
+        };
+#pragma unroll
+        for (int u = 0; u < E / 4; u++) {
+            const int e = tid + u * nthr;
+            const int rp = e & ((1 << LRP) - 1), k2 = e >> LRP;   // k2 in [0, H/2)
+            const float2* r0 = smem2 + (2 * rp) * a.SR;
+            const float2* r1 = r0 + a.SR;
+            float2 X0, X1, Y0, Y1;   // bin k2 (X) and bin H - k2 (Y; H/2 when k2 = 0)
+            if (k2 == 0) {
+                const float2 A0 = r0[0], A1 = r1[0];
+                X0 = make_float2(A0.x + A0.y, A0.x - A0.y);  // (X[0], X[N/2]) packed
+                X1 = make_float2(A1.x + A1.y, A1.x - A1.y);
+                const float2 th = __ldg(&twR[H / 2]);
+                const float2 B0 = r0[pad16(H / 2)], B1 = r1[pad16(H / 2)];
+                Y0 = split2(B0, B0, th);
+                Y1 = split2(B1, B1, th);
+            } else {
+                const float2 t1 = __ldg(&twR[k2]), t2 = __ldg(&twR[H - k2]);
+                const float2 A0 = r0[pad16(k2)], B0 = r0[pad16(H - k2)];
+                const float2 A1 = r1[pad16(k2)], B1 = r1[pad16(H - k2)];
+                X0 = split2(A0, B0, t1);
+                X1 = split2(A1, B1, t1);
+                Y0 = split2(B0, A0, t2);
+                Y1 = split2(B1, A1, t2);
+            }
+            const int k2m = k2 == 0 ? H / 2 : H - k2;
+            *reinterpret_cast<float4*>(out + (size_t)k2 * a.M + m0 + 2 * rp) = make_float4(X0.x, X0.y, X1.x, X1.y);
+            *reinterpret_cast<float4*>(out + (size_t)k2m * a.M + m0 + 2 * rp) = make_float4(Y0.x, Y0.y, Y1.x, Y1.y);
+        }
+    } else if constexpr (LG == 0 && LRPC >= 1) {
         // contiguous columns: rows 2 rp, 2 rp + 1 of bin k2 are adjacent -> one 16-byte store per pair
         constexpr int LRP = LRPC - 1;
 #pragma unroll

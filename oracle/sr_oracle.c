@@ -29,7 +29,14 @@
  *
  * Parity pins: every function is pinned by tests/test_oracle_*.py against
  * closed forms, brute force, numpy/scipy library routines or invariants
- * (DESIGN.md §4).  No function here is "parity unpinned".
+ * (DESIGN.md §4).  Round 1 claimed this while two branches were only pinned
+ * where they vanish: the fixed-point w update (Eq. 38) with beta != 0 and
+ * several passes, and the depth axis / third channel of the 3-D functions.
+ * Those pins were added in round 2 (test_oracle_wb.py::test_fixed_point_
+ * passes_*, test_oracle_3d.py::test_edge3_matches_scipy_*, ::test_axis_
+ * permutation_*), each checked to fail on an injected bug.  What has no
+ * external pin is the long-trajectory behaviour on C2-C5:
+ * the paper prints no values for those images.
  *
  * Compiled with -O2 -ffp-contract=off (no FMA contraction, no fast-math).
  * OpenMP parallelises only independent per-pixel / per-row loops, so results

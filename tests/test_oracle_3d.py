@@ -203,3 +203,85 @@ def test_plateau_fixed_point_and_clamp(orc):
     st = orc.init3(phi0)
     orc.iterate3(P, st, _rand(shape, 31, 0.2, 1.0), 2)
     assert np.abs(st["phi"]).max() <= 1.0
+
+
+# ----------------------------------------------------------------------------- depth axis and third channel
+def test_edge3_matches_scipy_gaussian_and_central_differences(orc):
+    """Eq. (1) in 3-D (Q16, Q26) against an independent library pipeline: scipy's separable
+    normalized Gaussian with replicate padding (mode="nearest", truncate=3 -> radius ceil(3 sigma)),
+    then central differences with replicate padding along all three axes."""
+    from scipy import ndimage
+    f = _rand((7, 9, 10), 40, 0.0, 1.0)
+    f[2:5, 3:7, 4:8] += 1.0                       # a block edge along every axis, incl. depth
+    for rho, s in ((30.0, 2), (5.0, 1)):
+        fs = ndimage.gaussian_filter(f, sigma=1.0, mode="nearest", truncate=3.0)
+        p = np.pad(fs, 1, mode="edge")
+        gz = (p[2:, 1:-1, 1:-1] - p[:-2, 1:-1, 1:-1]) / 2
+        gi = (p[1:-1, 2:, 1:-1] - p[1:-1, :-2, 1:-1]) / 2
+        gj = (p[1:-1, 1:-1, 2:] - p[1:-1, 1:-1, :-2]) / 2
+        m2 = gz ** 2 + gi ** 2 + gj ** 2
+        ref = 1.0 / (1.0 + rho * (m2 if s == 2 else np.sqrt(m2)))
+        assert np.allclose(orc.edge3(f, 1.0, rho, s), ref, rtol=0, atol=1e-12)
+        assert np.abs(gz).max() > 0.1               # the depth axis carries real signal
+
+
+_COMP_OF_AXIS = {1: 0, 2: 1, 0: 2}                 # array axis (z, i, j) -> component (1, 2, 3) = (i, j, z)
+
+
+def _perm_field(a, perm):
+    return np.ascontiguousarray(np.transpose(a, perm))
+
+
+def _perm_vec(v, perm):
+    """Permute a 3-vector field: new component along new axis a = old component along old axis perm[a]."""
+    out = [None, None, None]
+    for a in range(3):
+        out[_COMP_OF_AXIS[a]] = _perm_field(v[_COMP_OF_AXIS[perm[a]]], perm)
+    return tuple(out)
+
+
+@pytest.mark.parametrize("perm", [(0, 2, 1), (1, 0, 2), (2, 1, 0), (1, 2, 0)])
+def test_axis_permutation_commutes_with_every_3d_function(orc, perm):
+    """Metamorphic pin of the depth axis and the third channel (Q26: the 3-D operators are the 2-D
+    ones with an identical third axis): on a D = M = N cube, permuting the axes (and the vector
+    components with them) commutes with grad, div, the edge indicator, the ball / cube window sum,
+    the periodic solve, the RHS, the w/b update (threshold and fixed-point, BALL) and a full
+    iteration.  A wrong index, sign or weight on any one axis or channel breaks the symmetry."""
+    n = 6
+    sh = (n, n, n)
+    P = _p(2, d=1.7, beta=0.5)
+    psi = _rand(sh, 50, -1.2, 1.2)
+    w = tuple(_rand(sh, 51 + c) for c in range(3))
+    b = tuple(0.3 * _rand(sh, 54 + c) for c in range(3))
+    g = _rand(sh, 57, 0.1, 1.0)
+    pf = lambda a: _perm_field(a, perm)                                   # noqa: E731
+    pv = lambda v: _perm_vec(v, perm)                                     # noqa: E731
+    close = lambda a, r: np.allclose(a, r, rtol=0, atol=1e-12)            # noqa: E731
+    # grad / div
+    assert all(close(a, r) for a, r in zip(orc.grad3(pf(psi)), pv(orc.grad3(psi))))
+    assert close(orc.div3(*pv(w)), pf(orc.div3(*w)))
+    # edge indicator
+    img = _rand(sh, 58, 0.0, 1.0)
+    assert close(orc.edge3(pf(img), 1.0, 30.0, 2), pf(orc.edge3(img, 1.0, 30.0, 2)))
+    # window sums (ball and cube)
+    for shape in (0, 1):
+        assert all(close(a, r) for a, r in zip(orc.window_sum3(*pv(w), 2, 1.7, shape),
+                                               pv(orc.window_sum3(*w, 2, 1.7, shape))))
+    # solve (the 3-D symbol is symmetric in the axes when D = M = N)
+    F = _rand(sh, 59)
+    assert close(orc.solve3(pf(F), P["tau"], P["mu"]), pf(orc.solve3(F, P["tau"], P["mu"])))
+    # RHS
+    assert close(orc.rhs3(P, pf(psi), pv(w), pv(b), pf(g)), pf(orc.rhs3(P, psi, w, b, g)))
+    # w/b update, both modes
+    for over in (dict(), dict(w_mode=1, w_iters=2)):
+        Q = dict(P, **over)
+        nw, nb = orc.wb3(Q, pf(psi), pv(w), pv(b), pf(g))
+        rw, rb = orc.wb3(Q, psi, w, b, g)
+        assert all(close(a, r) for a, r in zip(nw + nb, pv(rw) + pv(rb)))
+    # one full iteration
+    st = {"phi": psi.copy(), "w": w, "b": b}
+    sp = {"phi": pf(psi), "w": pv(w), "b": pv(b)}
+    orc.iterate3(P, st, g, 1)
+    orc.iterate3(P, sp, pf(g), 1)
+    assert close(sp["phi"], pf(st["phi"]))
+    assert all(close(a, r) for a, r in zip(sp["w"] + sp["b"], pv(st["w"]) + pv(st["b"])))

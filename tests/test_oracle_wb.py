@@ -132,3 +132,58 @@ def test_fixed_point_mode(orc):
             den = P["gamma"] * s["g"][i, j] * orc.delta(s["phi"][i, j], P["epsilon"]) + P["mu"]
             assert w1[i, j] == pytest.approx(P["mu"] * (g1[i, j] + s["b1"][i, j]) / den, abs=1e-14)
             assert w2[i, j] == pytest.approx(P["mu"] * (g2[i, j] + s["b2"][i, j]) / den, abs=1e-14)
+
+
+def _fixed_point_reference(orc, P, phi, w1, w2, b1, b2, g, passes):
+    """Eq. (38)-(39) written out pass by pass from pinned pieces (orc.grad: Eq. 35; orc.h: Eq. 11;
+    orc.window_sum: P:368, pinned by impulse / full-window / locality in test_oracle_window.py):
+    w^{k+1,0} = w^k and, for r = 0..passes-1,
+        v^r    = sum_W G h(phi^{k+1}) w^{k+1,r}                           (Eq. 38)
+        w^{r+1} = (mu grad phi + mu b + 2 beta h v^r) / (gamma g delta + mu)   (Eq. 39)
+    with the NONE projection (Q1)."""
+    eps, l = P["epsilon"], P["l"]
+    hv = np.vectorize(lambda x: orc.h(x, eps, l))(phi)
+    dl = np.vectorize(lambda x: orc.delta(x, eps))(phi)
+    gp1, gp2 = orc.grad(phi)
+    n1, n2 = w1.copy(), w2.copy()
+    for _ in range(passes):
+        v1, v2 = orc.window_sum(hv * n1, hv * n2, P["window"], P["d"], P["window_shape"])
+        den = P["gamma"] * g * dl + P["mu"]
+        n1 = (P["mu"] * gp1 + P["mu"] * b1 + 2 * P["beta"] * hv * v1) / den
+        n2 = (P["mu"] * gp2 + P["mu"] * b2 + 2 * P["beta"] * hv * v2) / den
+    return n1, n2
+
+
+@pytest.mark.parametrize("passes", [1, 2, 3])
+def test_fixed_point_passes_recompute_v_from_the_previous_pass(orc, passes):
+    """NEXT-2 pin with beta != 0 and several passes: one impulse of w^k at the centre, phi = 0 where
+    h(0) = 1, gamma = 0.  Pass r+1 must use v^r built from w^{k+1,r} (Eq. 38), not from w^k: with the
+    impulse the two readings differ from the second pass on (the first pass spreads the impulse over
+    the window, the second spreads that again).  Also the gamma != 0 denominator on a random state."""
+    from synth import paper_params
+    M, N = 15, 13
+    phi = np.zeros((M, N))
+    w1, w2 = np.zeros((M, N)), np.zeros((M, N))
+    w1[7, 6], w2[7, 6] = 0.8, -0.5
+    b1, b2 = np.zeros((M, N)), np.zeros((M, N))
+    g = np.ones((M, N))
+    P = paper_params(3, gamma=0.0, beta=0.6, w_mode=1, w_iters=passes, w_proj=2)
+    n1, n2, nb1, nb2 = orc.wb(P, phi, w1, w2, b1, b2, g)
+    r1, r2 = _fixed_point_reference(orc, P, phi, w1, w2, b1, b2, g, passes)
+    assert np.allclose(n1, r1, atol=1e-14) and np.allclose(n2, r2, atol=1e-14)
+    gp1, gp2 = orc.grad(phi)
+    assert np.allclose(nb1, b1 + gp1 - n1, atol=1e-15) and np.allclose(nb2, b2 + gp2 - n2, atol=1e-15)
+    if passes >= 2:
+        # the reading "v^r from w^k" would give the one-pass result at every pass: it must differ
+        s1, s2 = _fixed_point_reference(orc, P, phi, w1, w2, b1, b2, g, 1)
+        assert np.max(np.abs(n1 - s1)) > 1e-3
+        # a pixel two window radii from the impulse: zero after one pass, reached only through w^{k+1,1}
+        assert s1[7, 12] == 0.0 and s1[7, 9] != 0.0
+        assert abs(n1[7, 12]) > 1e-6
+    # random state, gamma != 0, through the same reference
+    rng = np.random.default_rng(33)
+    s = _state(rng, 9, 11)
+    P = paper_params(2, beta=0.4, w_mode=1, w_iters=passes, w_proj=2)
+    n1, n2, _, _ = orc.wb(P, s["phi"], s["w1"], s["w2"], s["b1"], s["b2"], s["g"])
+    r1, r2 = _fixed_point_reference(orc, P, s["phi"], s["w1"], s["w2"], s["b1"], s["b2"], s["g"], passes)
+    assert np.allclose(n1, r1, atol=1e-13) and np.allclose(n2, r2, atol=1e-13)

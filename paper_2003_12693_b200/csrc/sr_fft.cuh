@@ -67,11 +67,11 @@ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
 }
 __device__ __forceinline__ float2 conjf2(float2 a) { return make_float2(a.x, -a.y); }
 
-// scale / symbol(k1, k2) with symbol = 1 + tau mu (cm + ck) in [1, 1 + 8 tau mu] (Eq. 32, Q10).  The
-// denominator is always a normal number >= 1, so the approximate reciprocal (MUFU.RCP, <= 2 ulp) replaces
-// the IEEE division and its slow-path check (~8 instructions per spectral coefficient).
+// scale / symbol(k1, k2) with symbol = 1 + tau mu (cm + ck) in [1, 1 + 8 tau mu] (Eq. 32, Q10).  scale =
+// 1 / (M N/2) is a power of two, so scale * rcp_rn(symbol) IS the IEEE quotient (correctly rounded, Q20)
+// at the cost of a correctly rounded reciprocal instead of a full division.
 __device__ __forceinline__ float sym_scale(float scale, float taumu, float cm, float ck) {
-    return __fdividef(scale, 1.f + taumu * (cm + ck));
+    return scale * __frcp_rn(1.f + taumu * (cm + ck));
 }
 
 __host__ __device__ constexpr int brevn(int k, int bits) {

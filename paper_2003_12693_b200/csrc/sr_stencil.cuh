@@ -38,12 +38,6 @@ struct Reg {
 //   h  = (2 - |a| + sinpi(|a|)/pi) / 2,           h' = -sign(a) (1 - cospi(a)) / (2 eps),
 //   delta = (1 + cospi(a)) / (2 eps) [|a| <= 1],  delta' = -(pi / (2 eps^2)) sinpi(a) [|a| <= 1],
 // and all four vanish for |a| >= 2 (only one of H(x +- l) is inside its band at a time).
-__device__ __forceinline__ float sqrt_approx(float x) {
-    float y;
-    asm("sqrt.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-
 __device__ __forceinline__ float H_of(float y, float s, const Reg& r) {   // Eq. (5), s = sinpi(y/eps)
     if (y > r.eps) return 1.f;
     if (y < -r.eps) return 0.f;
@@ -467,7 +461,7 @@ __device__ __forceinline__ void rhs_tile(float4* __restrict__ U, const float* __
             // neighbour differences first: exact (Sterbenz) for nearby values, so the O(1) level of
             // psi does not enter the rounding of the Laplacian
             const float lap = ((Pu[c] - ps) + (Pd[c] - ps)) + ((left - ps) + (right - ps));
-            const float wn = sqrt_approx(w1_[c] * w1_[c] + w2_[c] * w2_[c]);
+            const float wn = sqrtf(w1_[c] * w1_[c] + w2_[c] * w2_[c]);   // IEEE sqrt (Q20)
             const float wv = w1_[c] * v[i][c].x + w2_[c] * v[i][c].y;
             const RegVals rv = reg_all<LEQ>(ps, a.reg);
             const float t = -a.gamma * g_[c] * wn * rv.dp + a.alpha * g_[c] * rv.d + 2.f * a.beta * rv.hp * wv +
@@ -486,9 +480,9 @@ __device__ __forceinline__ void rhs_tile(float4* __restrict__ U, const float* __
 __device__ __forceinline__ void project_w(int mode, float& x, float& y) {
     const float n2 = x * x + y * y;
     if ((mode == 0 && n2 > 1.f) || (mode == 1 && n2 > 1e-8f)) {   // BALL: |w| > 1; SPHERE: |w| > 1e-4
-        const float inv = rsqrtf(n2);
-        x *= inv;
-        y *= inv;
+        const float n = sqrtf(n2);                                // IEEE sqrt and divides (Q20)
+        x = x / n;
+        y = y / n;
     }
 }
 
@@ -519,8 +513,8 @@ __device__ __forceinline__ void wb_pixel(const StencilArgs& a, float ps, float p
         const float t = a.gamma_mu * g * dd;
         const float nb2v = Bx * Bx + By * By;
         if (nb2v > 0.f) {
-            const float inv = rsqrtf(nb2v);              // 1/|B|
-            const float m = fmaxf(1.f - t * inv, 0.f);   // max(|B| - t, 0)/|B|
+            const float nb = sqrtf(nb2v);                // |B|, IEEE (Q20)
+            const float m = fmaxf(nb - t, 0.f) / nb;     // max(|B| - t, 0)/|B|, IEEE divide
             x = m * Bx;
             y = m * By;
         } else {
@@ -770,7 +764,7 @@ __device__ __forceinline__ void rhs_points_tma(const float* Ps, const float* W1s
                                 add2(sub2(make_float2(pl, P.x), P), sub2(make_float2(P.y, pr), P)));
         const float2 dv = sub2(add2(sub2(c1, c1u), c2), c2l);
         const float2 n2 = fma2(W1, W1, mul2(W2, W2));
-        const float2 wn = make_float2(sqrt_approx(n2.x), sqrt_approx(n2.y));
+        const float2 wn = make_float2(sqrtf(n2.x), sqrtf(n2.y));   // IEEE sqrt (Q20)
         const float2 wv = fma2(W1, make_float2(v[i][0].x, v[i][1].x), mul2(W2, make_float2(v[i][0].y, v[i][1].y)));
         float2 hp, dd, dp;
         reg_rhs2<LEQ>(P, a.reg, hp, dd, dp);

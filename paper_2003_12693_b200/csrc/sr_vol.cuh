@@ -214,10 +214,10 @@ __global__ void __launch_bounds__(256) k3_rhs(const float* __restrict__ phi, con
 __device__ __forceinline__ void project3(int mode, float& x, float& y, float& z) {
     const float n2 = x * x + y * y + z * z;
     if ((mode == 0 && n2 > 1.f) || (mode == 1 && n2 > 1e-8f)) {
-        const float inv = rsqrtf(n2);
-        x *= inv;
-        y *= inv;
-        z *= inv;
+        const float n = sqrtf(n2);   // IEEE sqrt and divides (Q20)
+        x = x / n;
+        y = y / n;
+        z = z / n;
     }
 }
 
@@ -259,7 +259,8 @@ __global__ void __launch_bounds__(256) k3_wb(const float* __restrict__ phi, cons
             const float t = a.gamma_mu * gg * dd;
             const float nb = B1 * B1 + B2 * B2 + B3 * B3;
             if (nb > 0.f) {
-                const float m = fmaxf(1.f - t * rsqrtf(nb), 0.f);
+                const float sn = sqrtf(nb);
+                const float m = fmaxf(sn - t, 0.f) / sn;   // IEEE (Q20)
                 n1 = m * B1;
                 n2 = m * B2;
                 n3 = m * B3;

@@ -117,6 +117,22 @@ sr_status sr_sb_create_dist(const sr_sb_params* p, int device, void* stream, con
 /* Rows per image held in the caller-visible buffers of this context (M, or M/P for an NCCL slab). */
 int sr_sb_local_rows(const sr_sb_ctx* ctx);
 
+/* The slab exchange schedule (host-only, needs no GPU).  Both slab backends execute
+ * exactly these per-rank lists of point-to-point ops: NCCL as grouped ncclSend / ncclRecv, the
+ * LOCAL group as device copies pairing the k-th send from r to d with the k-th receive on d from r
+ * (NCCL's per-peer order).  kind 0: ghost rows of one channel plane with the periodic wrap rows
+ * (phi, Eq. 32); 1: ghost rows without wrap (w, b, image); 2 / 3: chunk k of nk of the forward /
+ * backward spectrum all-to-all of an M/P x N slab.  Writes 5 int64 per op to `ops`
+ * (if non-NULL, at most max_ops): send (1) or receive (0), peer rank, buffer (halo: channel 0;
+ * a2a: 0 = the row-pass spectrum [H/G][M/P][G], 1 = the column buffer [P][H/(P G)][M/P][G]),
+ * offset and count in floats (halo offsets are relative to local row 0, the top ghost rows are
+ * negative).  Returns the number of ops, or -1 on bad arguments (P, r, Ml >= 1, gh >= 1, 0 <= k < nk,
+ * (N/2) % P == 0 and the chunk dividing the block). */
+int sr_sb_slab_schedule(int kind, int P, int r, int Ml, int gh, int N, int k, int nk, long long* ops, int max_ops);
+/* Spectrum all-to-all chunks this slab context pipelines with its column solve (1 = unchunked;
+ * SRSB_A2A_CHUNKS overrides the default 4 at creation). */
+int sr_sb_a2a_chunks(const sr_sb_ctx* ctx);
+
 /* Algorithm 1 step (1): image f and initial level set phi0 ([batch][M][N]) ->
  * g (Eq. 1), phi = phi0, w = grad phi0 (Q12), b = 0.  Resets k to 0. */
 sr_status sr_sb_set_image(sr_sb_ctx* ctx, const float* image, const float* phi0);

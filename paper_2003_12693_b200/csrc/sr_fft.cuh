@@ -318,7 +318,16 @@ struct FftColArgs {
     long long seg_stride;  // complex elements between segments
     long long bstride;     // complex elements between images
     int k2_off;     // global index of local column 0 (slab: rank * H / P)
+    const float* sym;   // [H + 1][M] table of scale / symbol(k1, k2), fp64-computed and rounded once
+                        // (L2-resident, shared by the batch); null: sym_scale
 };
+
+// scale / symbol(k1, k2): from the table when the context has one, else the correctly rounded
+// reciprocal of the fp32 symbol
+__device__ __forceinline__ float sym_at(const FftColArgs& a, const float* __restrict__ cM, int M, int k1, int k2,
+                                        float ck) {
+    return a.sym ? __ldg(&a.sym[(size_t)k2 * M + k1]) : sym_scale(a.scale, a.taumu, __ldg(&cM[k1]), ck);
+}
 
 // Column pass: forward FFT, divide by the symbol, inverse FFT, in place.  Threads of one column
 // are consecutive (t fastest), so a warp works inside one transform.
@@ -367,9 +376,8 @@ __global__ void __maxnreg__(LOGM >= 12 ? SRSB_COLS_MAXNREG_BIG : SRSB_COLS_MAXNR
                 const int k1 = t + u * T;
                 const float2 C = v[u];
                 const float2 Cc = conjf2(sm[pad16((M - k1) & (M - 1))]);
-                const float cm = __ldg(&cM[k1]);
-                const float s0 = sym_scale(a.scale, a.taumu, cm, c0);
-                const float sh = sym_scale(a.scale, a.taumu, cm, ch);
+                const float s0 = sym_at(a, cM, M, k1, 0, c0);
+                const float sh = sym_at(a, cM, M, k1, a.H, ch);
                 const float p = 0.5f * (s0 + sh), m = 0.5f * (s0 - sh);
                 v[u] = make_float2(p * C.x + m * Cc.x, p * C.y + m * Cc.y);
             }
@@ -377,7 +385,7 @@ __global__ void __maxnreg__(LOGM >= 12 ? SRSB_COLS_MAXNREG_BIG : SRSB_COLS_MAXNR
             const float ck = __ldg(&cN[k2]);
 #pragma unroll
             for (int u = 0; u < E; u++) {
-                const float s = sym_scale(a.scale, a.taumu, __ldg(&cM[t + u * T]), ck);
+                const float s = sym_at(a, cM, M, t + u * T, k2, ck);
                 v[u] = make_float2(v[u].x * s, v[u].y * s);
             }
         }
@@ -386,7 +394,7 @@ __global__ void __maxnreg__(LOGM >= 12 ? SRSB_COLS_MAXNREG_BIG : SRSB_COLS_MAXNR
         const float ck = __ldg(&cN[k2]);
 #pragma unroll
         for (int u = 0; u < E; u++) {
-            const float s = sym_scale(a.scale, a.taumu, __ldg(&cM[t + u * T]), ck);
+            const float s = sym_at(a, cM, M, t + u * T, k2, ck);
             v[u] = make_float2(v[u].x * s, v[u].y * s);
         }
     }
@@ -447,9 +455,8 @@ __global__ void __launch_bounds__(512, 1) k_cols_solve_p(float2* __restrict__ sp
                 const int k1 = t + u * T;
                 const float2 C = v[u];
                 const float2 Cc = conjf2(sm[pad16((M - k1) & (M - 1))]);
-                const float cm = __ldg(&cM[k1]);
-                const float s0 = sym_scale(a.scale, a.taumu, cm, c0);
-                const float sh = sym_scale(a.scale, a.taumu, cm, ch);
+                const float s0 = sym_at(a, cM, M, k1, 0, c0);
+                const float sh = sym_at(a, cM, M, k1, a.H, ch);
                 const float pp = 0.5f * (s0 + sh), mm = 0.5f * (s0 - sh);
                 v[u] = make_float2(pp * C.x + mm * Cc.x, pp * C.y + mm * Cc.y);
             }
@@ -458,7 +465,7 @@ __global__ void __launch_bounds__(512, 1) k_cols_solve_p(float2* __restrict__ sp
             const float ck = __ldg(&cN[k2]);
 #pragma unroll
             for (int u = 0; u < E; u++) {
-                const float sc = sym_scale(a.scale, a.taumu, __ldg(&cM[t + u * T]), ck);
+                const float sc = sym_at(a, cM, M, t + u * T, k2, ck);
                 v[u] = make_float2(v[u].x * sc, v[u].y * sc);
             }
         }

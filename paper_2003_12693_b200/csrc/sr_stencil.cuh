@@ -461,9 +461,10 @@ __device__ __forceinline__ void rhs_tile(float4* __restrict__ U, const float* __
             // neighbour differences first: exact (Sterbenz) for nearby values, so the O(1) level of
             // psi does not enter the rounding of the Laplacian
             const float lap = ((Pu[c] - ps) + (Pd[c] - ps)) + ((left - ps) + (right - ps));
-            const float wn = sqrtf(w1_[c] * w1_[c] + w2_[c] * w2_[c]);   // IEEE sqrt (Q20)
             const float wv = w1_[c] * v[i][c].x + w2_[c] * v[i][c].y;
             const RegVals rv = reg_all<LEQ>(ps, a.reg);
+            // |w| (IEEE sqrt, Q20) only where delta' != 0: elsewhere its product with delta' is 0
+            const float wn = rv.dp != 0.f ? sqrtf(w1_[c] * w1_[c] + w2_[c] * w2_[c]) : 0.f;
             const float t = -a.gamma * g_[c] * wn * rv.dp + a.alpha * g_[c] * rv.d + 2.f * a.beta * rv.hp * wv +
                             a.mu * dv;
             out[c] = a.aos ? ps + a.tau * t : a.tau * (t + a.mu * lap);
@@ -512,7 +513,10 @@ __device__ __forceinline__ void wb_pixel(const StencilArgs& a, float ps, float p
         const float By = gp2 + b2 + a.beta2_mu * hh * v.y;
         const float t = a.gamma_mu * g * dd;
         const float nb2v = Bx * Bx + By * By;
-        if (nb2v > 0.f) {
+        if (t == 0.f) {                                  // off the band (delta = 0): the shrink is the
+            x = Bx;                                      // identity, exactly what the IEEE form below
+            y = By;                                      // gives there ((|B| - 0)/|B| = 1)
+        } else if (nb2v > 0.f) {
             const float nb = sqrtf(nb2v);                // |B|, IEEE (Q20)
             const float m = fmaxf(nb - t, 0.f) / nb;     // max(|B| - t, 0)/|B|, IEEE divide
             x = m * Bx;
@@ -763,11 +767,13 @@ __device__ __forceinline__ void rhs_points_tma(const float* Ps, const float* W1s
         const float2 lap = add2(add2(sub2(Pu, P), sub2(Pd, P)),
                                 add2(sub2(make_float2(pl, P.x), P), sub2(make_float2(P.y, pr), P)));
         const float2 dv = sub2(add2(sub2(c1, c1u), c2), c2l);
-        const float2 n2 = fma2(W1, W1, mul2(W2, W2));
-        const float2 wn = make_float2(sqrtf(n2.x), sqrtf(n2.y));   // IEEE sqrt (Q20)
         const float2 wv = fma2(W1, make_float2(v[i][0].x, v[i][1].x), mul2(W2, make_float2(v[i][0].y, v[i][1].y)));
         float2 hp, dd, dp;
         reg_rhs2<LEQ>(P, a.reg, hp, dd, dp);
+        // |w| (IEEE sqrt, Q20) only where delta' != 0 (the band): elsewhere its product with delta' is 0
+        float2 wn = f2(0.f);
+        if (dp.x != 0.f) wn.x = sqrtf(fmaf(W1.x, W1.x, W2.x * W2.x));
+        if (dp.y != 0.f) wn.y = sqrtf(fmaf(W1.y, W1.y, W2.y * W2.y));
         // t = g (alpha delta - gamma |w| delta') + 2 beta h' w.v + mu div(b - w)
         float2 t = mul2(Gv, fma2(f2(a.alpha), dd, mul2(f2(-a.gamma), mul2(wn, dp))));
         t = fma2(f2(2.f * a.beta), mul2(hp, wv), t);

@@ -58,6 +58,12 @@ struct sr_sb_ctx {
     long long pitch = 0;           // floats per image plane (Ml + 2 gh) * N
     std::vector<sr_sb_ctx*> members;   // LOCAL group leader: the slab contexts (leader has no fields)
     ncclComm_t comm = nullptr;
+    // slab exchanges: a comm stream and fork/join events so the all-to-all of column chunk k + 1
+    // overlaps the column solve of chunk k; a2a_chunks = 1: no pipelining
+    cudaStream_t sc = nullptr;
+    static constexpr int kMaxChunks = 8;
+    cudaEvent_t xev[2 * kMaxChunks + 2] = {};
+    int a2a_chunks = 1;
     // fields: *_base = allocation, field = base + gh * N (local row 0 of image 0)
     float *phi_base = nullptr, *F_base = nullptr, *w_base[2] = {nullptr, nullptr}, *b_base = nullptr,
           *g_base = nullptr;
@@ -66,12 +72,12 @@ struct sr_sb_ctx {
     float2* spec_cols = nullptr;   // slab: [P][H/(P G)][Ml][G] (all-to-all receive buffer)
     float2 *twH = nullptr, *twM = nullptr, *twR = nullptr;
     float *cM = nullptr, *cN = nullptr;
+    float* sym = nullptr;          // [H + 1][M] scale / symbol table (FftColArgs::sym), when small enough
     int* flag = nullptr;
     int wcur = 0;
     long long k = 0;
     bool have_state = false;
-    cudaGraphExec_t graph = nullptr;
-    int graph_wcur = -1;
+    cudaGraphExec_t graph[2] = {nullptr, nullptr};   // captured kGraphIters iterations, per w ping-pong parity
     std::string err;
     // launch configuration
     RowKernel rfwd = nullptr;
@@ -289,6 +295,13 @@ sr_status configure(sr_sb_ctx* c) {
         c->cols_p = (!c->slab && G == 1 && !(ev && ev[0] == '0')) ? pick_col_p(lgM) : nullptr;
     }
     c->cgrid = dim3(Hl / cpc, B, 1);
+    if (c->slab) {   // all-to-all chunks (column groups) pipelined with the column solve; SRSB_A2A_CHUNKS
+        int nk = 4;
+        if (const char* ev = std::getenv("SRSB_A2A_CHUNKS")) nk = std::atoi(ev);
+        const int unit = std::max(G, cpc);   // a chunk holds whole column groups and whole column CTAs
+        while (nk > 1 && (!is_pow2(nk) || nk > sr_sb_ctx::kMaxChunks || Hl / nk < unit || (Hl / nk) % unit)) nk--;
+        c->a2a_chunks = std::max(nk, 1);
+    }
     c->cblock = dim3(cpc * T_m, 1, 1);
     c->csmem = cpc * c->ca.SC * (int)sizeof(float2);
     // stencils
@@ -393,6 +406,16 @@ sr_status make_tables(sr_sb_ctx* c) {
     CK(cudaMemcpyAsync(c->twR, twR.data(), H * sizeof(float2), cudaMemcpyHostToDevice, c->s));
     CK(cudaMemcpyAsync(c->cM, cM.data(), M * sizeof(float), cudaMemcpyHostToDevice, c->s));
     CK(cudaMemcpyAsync(c->cN, cN.data(), (H + 1) * sizeof(float), cudaMemcpyHostToDevice, c->s));
+    if (c->sym) {   // scale / symbol(k1, k2) of Eq. (32) in fp64, rounded once to fp32 (Q10, Q20)
+        std::vector<float> sym((size_t)(H + 1) * M);
+        const double tm = (double)c->p.tau * (double)c->p.mu, scale = 1.0 / ((double)M * (double)H);
+        for (int k2 = 0; k2 <= H; k2++)
+            for (int k1 = 0; k1 < M; k1++)
+                sym[(size_t)k2 * M + k1] = (float)(scale / (1.0 + tm * (4.0 - 2.0 * std::cos(2 * pi * k1 / M) -
+                                                                        2.0 * std::cos(2 * pi * k2 / N))));
+        CK(cudaMemcpyAsync(c->sym, sym.data(), sym.size() * sizeof(float), cudaMemcpyHostToDevice, c->s));
+    }
+    c->ca.sym = c->sym;
     if (c->p.phi_solver == SR_PHI_AOS) {   // LR factors once, fp64 -> fp32
         auto factors = [&](int n, std::vector<float>& cp, std::vector<float>& r) {
             const double cc = 2.0 * (double)c->p.tau * (double)c->p.mu, a = -cc;
@@ -454,6 +477,16 @@ void enq_cols(sr_sb_ctx* c) {
                                                          c->ca);
     prof_end(c, SR_K_COLS_SOLVE);
 }
+// slab mode: the column solve of chunk k of nk (columns [k, k+1) Hl/nk of this slab), on stream st
+void enq_cols_chunk(sr_sb_ctx* c, int k, int nk, cudaStream_t st) {
+    const int Hl = c->p.N / 2 / c->nranks, Hk = Hl / nk;
+    FftColArgs ca = c->ca;
+    ca.k2_off += k * Hk;
+    prof_begin(c);
+    c->cols<<<dim3(Hk >> ca.lg_cpc, 1, 1), c->cblock, c->csmem, st>>>(c->spec_cols + (size_t)k * Hk * c->Ml, c->twM,
+                                                                       c->cM, c->cN, ca);
+    prof_end(c, SR_K_COLS_SOLVE);
+}
 void enq_c2r(sr_sb_ctx* c, float* out, float clip, int accum, int sweep = -1) {
     FftRowArgs ra = c->ra_inv;
     ra.accum = accum;
@@ -500,90 +533,124 @@ float* field_rows(sr_sb_ctx* c, int f, int ch) {
     }
 }
 
-// Ghost-row exchange of field f between the slabs `m` (all slabs for LOCAL, this one for NCCL):
-// A: last gh rows of slab r -> top ghost of r+1;  B: first gh rows of r -> bottom ghost of r-1;
-// C (wrap = phi: the periodic Laplacian rows of Eq. (32)): last rows of P-1 -> top ghost of 0,
-// first rows of 0 -> bottom ghost of P-1.  Same phase order on every rank (NCCL pair matching).
-sr_status halo(std::vector<sr_sb_ctx*>& m, int f, bool wrap) {
+// ---- the exchange schedule (host-only; no CUDA): one list of point-to-point ops per rank.  Both
+// backends execute exactly these lists -- NCCL as grouped ncclSend / ncclRecv, LOCAL as device
+// copies pairing the k-th send from r to d with the k-th receive on d from r (NCCL's per-peer FIFO
+// matching) -- and sr_sb_slab_schedule exports them so the CPU tests can run the same lists across
+// processes (gloo) and check every offset, count and pairing without a GPU.
+struct XOp {
+    int send;         // 1 send, 0 receive
+    int peer;         // the other rank
+    int buf;          // halo: channel of the field; a2a: 0 = row-pass spectrum, 1 = column buffer
+    long long off;    // elements from the buffer's base (halo: local row 0 of the channel plane)
+    long long cnt;    // elements
+};
+
+// Ghost rows of one channel plane: A: last gh rows of r -> top ghost of r+1; B: first gh rows of r
+// -> bottom ghost of r-1; C (wrap = phi, the periodic Laplacian rows of Eq. (32)): last rows of P-1
+// -> top ghost of 0, first rows of 0 -> bottom ghost of P-1.  Same phase order on every rank.
+void halo_ops(int P, int r, int Ml, int gh, int N, bool wrap, int ch, std::vector<XOp>& ops) {
+    const long long cnt = (long long)gh * N, top = -(long long)gh * N, bot = (long long)Ml * N,
+                    last = (long long)(Ml - gh) * N;
+    if (r + 1 < P) ops.push_back({1, r + 1, ch, last, cnt});
+    if (r > 0) ops.push_back({0, r - 1, ch, top, cnt});
+    if (r > 0) ops.push_back({1, r - 1, ch, 0, cnt});
+    if (r + 1 < P) ops.push_back({0, r + 1, ch, bot, cnt});
+    if (wrap) {
+        if (r == P - 1) ops.push_back({1, 0, ch, last, cnt});
+        if (r == 0) ops.push_back({0, P - 1, ch, top, cnt});
+        if (r == 0) ops.push_back({1, P - 1, ch, 0, cnt});
+        if (r == P - 1) ops.push_back({0, 0, ch, bot, cnt});
+    }
+}
+
+// Spectrum transpose, chunk `k` of `nk`: the row pass leaves slab r's spectrum as [H/G][Ml][G], so
+// the columns [d H/P, (d+1) H/P) bound for slab d are one contiguous block of blk = (H/P) Ml
+// complex; chunk k is the contiguous sub-block of its columns [k, k+1) (H/P)/nk, sub = blk / nk.
+// Slab d stores the block from src as segment src of its column buffer [P][H/(P G)][Ml][G]
+// (offset src blk + k sub).  fwd: spectrum -> column buffer; bwd: the reverse.  Counts in floats.
+void a2a_ops(int P, int r, long long blk, int k, int nk, bool fwd, std::vector<XOp>& ops) {
+    const long long sub = blk / nk;
+    for (int d = 0; d < P; d++) {
+        // send to d its block, receive from d our segment d (same chunk of the same columns)
+        const long long soff = (long long)d * blk + (long long)k * sub;
+        ops.push_back({1, d, fwd ? 0 : 1, 2 * soff, 2 * sub});
+        ops.push_back({0, d, fwd ? 1 : 0, 2 * soff, 2 * sub});
+    }
+}
+
+// plane pointer (local row 0) of channel ch of field f (B = 1 in slab mode)
+float* xbuf(sr_sb_ctx* c, int f, int buf) {
+    if (f < 0) return reinterpret_cast<float*>(buf == 0 ? c->spec : c->spec_cols);
+    return field_rows(c, f, buf);
+}
+
+// Execute per-rank op lists.  LOCAL: ops[r] for every slab r of `m`; NCCL: ops[0] for this rank.
+sr_status run_ops(std::vector<sr_sb_ctx*>& m, int f, const std::vector<std::vector<XOp>>& ops, cudaStream_t st) {
     sr_sb_ctx* c = m[0];
-    const int P = c->nranks, gh = c->gh, N = c->p.N, Ml = c->Ml;
-    const int nch = (f == HF_W || f == HF_B) ? 2 : 1;
-    const size_t cnt = (size_t)gh * N;
     if (c->backend == BK_LOCAL) {
-        for (int ch = 0; ch < nch; ch++)
-            for (int r = 0; r < P; r++) {
-                sr_sb_ctx* x = m[r];
-                float* rows = field_rows(x, f, ch);
-                if (r + 1 < P) CK(cudaMemcpyAsync(field_rows(m[r + 1], f, ch) - cnt, rows + (size_t)(Ml - gh) * N,
-                                                  cnt * 4, cudaMemcpyDeviceToDevice, x->s));
-                if (r > 0) CK(cudaMemcpyAsync(field_rows(m[r - 1], f, ch) + (size_t)Ml * N, rows, cnt * 4,
-                                              cudaMemcpyDeviceToDevice, x->s));
-                if (wrap && r == P - 1)
-                    CK(cudaMemcpyAsync(field_rows(m[0], f, ch) - cnt, rows + (size_t)(Ml - gh) * N, cnt * 4,
-                                       cudaMemcpyDeviceToDevice, x->s));
-                if (wrap && r == 0)
-                    CK(cudaMemcpyAsync(field_rows(m[P - 1], f, ch) + (size_t)Ml * N, rows, cnt * 4,
-                                       cudaMemcpyDeviceToDevice, x->s));
+        const int P = (int)m.size();
+        // recv queues per (dst, src) pair in program order
+        std::vector<std::vector<size_t>> nxt(P * P, std::vector<size_t>());
+        for (int d = 0; d < P; d++)
+            for (size_t i = 0; i < ops[d].size(); i++)
+                if (!ops[d][i].send) nxt[d * P + ops[d][i].peer].push_back(i);
+        std::vector<size_t> used(P * P, 0);
+        for (int r = 0; r < P; r++)
+            for (const XOp& o : ops[r]) {
+                if (!o.send) continue;
+                const int d = o.peer;
+                auto& q = nxt[d * P + r];
+                size_t& u = used[d * P + r];
+                if (u >= q.size()) return fail(c, SR_ERR_STATE, "slab schedule: a send without a matching receive");
+                const XOp& rv = ops[d][q[u++]];
+                if (rv.cnt != o.cnt) return fail(c, SR_ERR_STATE, "slab schedule: send/receive counts differ");
+                CK(cudaMemcpyAsync(xbuf(m[d], f, rv.buf) + rv.off, xbuf(m[r], f, o.buf) + o.off,
+                                   (size_t)o.cnt * sizeof(float), cudaMemcpyDeviceToDevice, st));
             }
+        for (int i = 0; i < P * P; i++)
+            if (used[i] != nxt[i].size()) return fail(c, SR_ERR_STATE, "slab schedule: a receive without a send");
         return SR_OK;
     }
     if (c->backend == BK_NCCL) {
-        const int r = c->rank;
-        if (P == 1) {   // a one-rank communicator: only the wrap rows, as local copies
-            if (wrap)
-                for (int ch = 0; ch < nch; ch++) {
-                    float* rows = field_rows(c, f, ch);
-                    CK(cudaMemcpyAsync(rows - cnt, rows + (size_t)(Ml - gh) * N, cnt * 4, cudaMemcpyDeviceToDevice, c->s));
-                    CK(cudaMemcpyAsync(rows + (size_t)Ml * N, rows, cnt * 4, cudaMemcpyDeviceToDevice, c->s));
-                }
+        const std::vector<XOp>& L = ops[0];
+        if (c->nranks == 1) {   // a one-rank communicator: self pairs as local copies (FIFO order)
+            std::vector<const XOp*> sends, recvs;
+            for (const XOp& o : L) (o.send ? sends : recvs).push_back(&o);
+            if (sends.size() != recvs.size()) return fail(c, SR_ERR_STATE, "slab schedule: unpaired self op");
+            for (size_t i = 0; i < sends.size(); i++)
+                CK(cudaMemcpyAsync(xbuf(c, f, recvs[i]->buf) + recvs[i]->off, xbuf(c, f, sends[i]->buf) + sends[i]->off,
+                                   (size_t)sends[i]->cnt * sizeof(float), cudaMemcpyDeviceToDevice, st));
             return SR_OK;
         }
         NK(ncclGroupStart());
-        for (int ch = 0; ch < nch; ch++) {
-            float* rows = field_rows(c, f, ch);
-            // A
-            if (r + 1 < P) NK(ncclSend(rows + (size_t)(Ml - gh) * N, cnt, ncclFloat, r + 1, c->comm, c->s));
-            if (r > 0) NK(ncclRecv(rows - cnt, cnt, ncclFloat, r - 1, c->comm, c->s));
-            // B
-            if (r > 0) NK(ncclSend(rows, cnt, ncclFloat, r - 1, c->comm, c->s));
-            if (r + 1 < P) NK(ncclRecv(rows + (size_t)Ml * N, cnt, ncclFloat, r + 1, c->comm, c->s));
-            // C
-            if (wrap) {
-                if (r == P - 1) NK(ncclSend(rows + (size_t)(Ml - gh) * N, cnt, ncclFloat, 0, c->comm, c->s));
-                if (r == 0) NK(ncclRecv(rows - cnt, cnt, ncclFloat, P - 1, c->comm, c->s));
-                if (r == 0) NK(ncclSend(rows, cnt, ncclFloat, P - 1, c->comm, c->s));
-                if (r == P - 1) NK(ncclRecv(rows + (size_t)Ml * N, cnt, ncclFloat, 0, c->comm, c->s));
-            }
+        for (const XOp& o : L) {
+            float* p = xbuf(c, f, o.buf) + o.off;
+            if (o.send) NK(ncclSend(p, (size_t)o.cnt, ncclFloat, o.peer, c->comm, st));
+            else NK(ncclRecv(p, (size_t)o.cnt, ncclFloat, o.peer, c->comm, st));
         }
         NK(ncclGroupEnd());
     }
     return SR_OK;
 }
 
-// Spectrum transpose between the row pass and the column pass (fwd) and back (bwd): slab r's
-// block of columns [d H/P, (d+1) H/P) (contiguous in [H/G][Ml][G]) goes to slab d, which stores
-// the P row blocks of its columns as P segments.
-sr_status alltoall(std::vector<sr_sb_ctx*>& m, bool fwd) {
+sr_status halo(std::vector<sr_sb_ctx*>& m, int f, bool wrap) {
     sr_sb_ctx* c = m[0];
-    const int P = c->nranks;
-    const size_t blk = (size_t)(c->p.N / 2 / P) * c->Ml;   // complex per (src, dst) pair
-    if (c->backend == BK_LOCAL) {
-        for (int src = 0; src < P; src++)
-            for (int dst = 0; dst < P; dst++) {
-                if (fwd)
-                    CK(cudaMemcpyAsync(m[dst]->spec_cols + src * blk, m[src]->spec + dst * blk, blk * sizeof(float2),
-                                       cudaMemcpyDeviceToDevice, m[src]->s));
-                else
-                    CK(cudaMemcpyAsync(m[src]->spec + dst * blk, m[dst]->spec_cols + src * blk, blk * sizeof(float2),
-                                       cudaMemcpyDeviceToDevice, m[src]->s));
-            }
-        return SR_OK;
-    }
-    if (c->backend == BK_NCCL) {
-        if (fwd) NK(ncclAlltoAll(c->spec, c->spec_cols, 2 * blk, ncclFloat, c->comm, c->s));
-        else NK(ncclAlltoAll(c->spec_cols, c->spec, 2 * blk, ncclFloat, c->comm, c->s));
-    }
-    return SR_OK;
+    const int nch = (f == HF_W || f == HF_B) ? 2 : 1;
+    std::vector<std::vector<XOp>> ops(m.size());
+    for (size_t i = 0; i < m.size(); i++)
+        for (int ch = 0; ch < nch; ch++)
+            halo_ops(c->nranks, m[i]->rank, c->Ml, c->gh, c->p.N, wrap, ch, ops[i]);
+    return run_ops(m, f, ops, c->s);
+}
+
+// Spectrum transpose chunk k of nk between the row pass and the column pass (fwd) and back (bwd).
+sr_status alltoall(std::vector<sr_sb_ctx*>& m, bool fwd, int k, int nk, cudaStream_t st) {
+    sr_sb_ctx* c = m[0];
+    const long long blk = (long long)(c->p.N / 2 / c->nranks) * c->Ml;   // complex per (src, dst) pair
+    std::vector<std::vector<XOp>> ops(m.size());
+    for (size_t i = 0; i < m.size(); i++) a2a_ops(c->nranks, m[i]->rank, blk, k, nk, fwd, ops[i]);
+    return run_ops(m, -1, ops, st);
 }
 
 // ------------------------------------------------------------------ the iteration
@@ -635,18 +702,50 @@ sr_status enq_iteration(sr_sb_ctx* c) {   // whole-image context
     return SR_OK;
 }
 
-// slab schedule over the member contexts
+// slab schedule over the member contexts.  The phi solve of each sweep runs
+//   r2c -> [all-to-all chunk 0 .. nk-1 on the comm stream] -> per chunk k: wait chunk k, column solve
+//   of chunk k on the work stream, then its backward all-to-all on the comm stream -> join -> c2r,
+// so the transfer of chunk k + 1 (and the return of chunk k - 1) overlaps the column solve of chunk k.
+sr_status slab_phi_solve(std::vector<sr_sb_ctx*>& m, float clip) {
+    sr_sb_ctx* c0 = m[0];
+    for (auto* x : m) enq_r2c(x, x->F);
+    const int nk = c0->a2a_chunks;
+    if (nk <= 1) {
+        RET(alltoall(m, true, 0, 1, c0->s));
+        for (auto* x : m) enq_cols_chunk(x, 0, 1, c0->s);
+        RET(alltoall(m, false, 0, 1, c0->s));
+    } else {
+        sr_sb_ctx* c = c0;
+        cudaEvent_t* fwd = c0->xev + 1;
+        cudaEvent_t* col = c0->xev + 1 + nk;
+        cudaEvent_t fork = c0->xev[0], join = c0->xev[2 * sr_sb_ctx::kMaxChunks + 1];
+        CK(cudaEventRecord(fork, c0->s));
+        CK(cudaStreamWaitEvent(c0->sc, fork, 0));
+        for (int k = 0; k < nk; k++) {
+            RET(alltoall(m, true, k, nk, c0->sc));
+            CK(cudaEventRecord(fwd[k], c0->sc));
+        }
+        for (int k = 0; k < nk; k++) {
+            CK(cudaStreamWaitEvent(c0->s, fwd[k], 0));
+            for (auto* x : m) enq_cols_chunk(x, k, nk, c0->s);
+            CK(cudaEventRecord(col[k], c0->s));
+            CK(cudaStreamWaitEvent(c0->sc, col[k], 0));
+            RET(alltoall(m, false, k, nk, c0->sc));
+        }
+        CK(cudaEventRecord(join, c0->sc));
+        CK(cudaStreamWaitEvent(c0->s, join, 0));
+    }
+    for (auto* x : m) enq_c2r(x, x->phi, clip, 1);
+    return SR_OK;
+}
+
 sr_status slab_iteration(std::vector<sr_sb_ctx*>& m) {
     sr_sb_ctx* c0 = m[0];
     const sr_sb_params& p = c0->p;
     for (int s = 0; s < p.S; s++) {
         RET(halo(m, HF_PHI, true));
         for (auto* x : m) enq_rhs(x, x->F);
-        for (auto* x : m) enq_r2c(x, x->F);
-        RET(alltoall(m, true));
-        for (auto* x : m) enq_cols(x);
-        RET(alltoall(m, false));
-        for (auto* x : m) enq_c2r(x, x->phi, (s == p.S - 1) ? p.phi_clip : 0.f, 1);
+        RET(slab_phi_solve(m, (s == p.S - 1) ? p.phi_clip : 0.f));
     }
     RET(halo(m, HF_PHI, true));
     const int passes = p.w_mode == SR_W_FIXED_POINT ? p.w_iters : 1;
@@ -733,6 +832,10 @@ sr_status create_one(const sr_sb_params* p, int device, cudaStream_t stream, int
     }
     ok = ok && cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming) == cudaSuccess &&
          cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming) == cudaSuccess;
+    if (ok && c->slab) {
+        ok = cudaStreamCreateWithFlags(&c->sc, cudaStreamNonBlocking) == cudaSuccess;
+        for (auto& e : c->xev) ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+    }
     if (!ok) { g_create_err = "stream/event creation failed"; sr_sb_destroy(c); return SR_ERR_CUDA; }
     ok = alloc((void**)&c->phi_base, nplane * 4) && alloc((void**)&c->F_base, nplane * 4) &&
          alloc((void**)&c->w_base[0], 2 * nplane * 4) && alloc((void**)&c->w_base[1], 2 * nplane * 4) &&
@@ -742,6 +845,11 @@ sr_status create_one(const sr_sb_params* p, int device, cudaStream_t stream, int
          alloc((void**)&c->cM, p->M * sizeof(float)) && alloc((void**)&c->cN, (p->N / 2 + 1) * sizeof(float)) &&
          alloc((void**)&c->flag, sizeof(int));
     if (ok && c->slab) ok = alloc((void**)&c->spec_cols, nspec * sizeof(float2));
+    {   // the symbol table when it stays L2-resident (<= 16 MB; SRSB_SYMTAB=0: the reciprocal path)
+        const size_t nsym = (size_t)(p->N / 2 + 1) * p->M;
+        const char* ev = std::getenv("SRSB_SYMTAB");
+        if (ok && nsym <= ((size_t)4 << 20) && !(ev && ev[0] == '0')) ok = alloc((void**)&c->sym, nsym * sizeof(float));
+    }
     if (ok && p->phi_solver == SR_PHI_AOS)
         ok = alloc((void**)&c->aos_cpM, p->M * 4) && alloc((void**)&c->aos_rM, p->M * 4) &&
              alloc((void**)&c->aos_cpN, p->N * 4) && alloc((void**)&c->aos_rN, p->N * 4);
@@ -990,19 +1098,37 @@ sr_status sr_sb_set_image(sr_sb_ctx* c, const float* image, const float* phi0) {
     return SR_OK;
 }
 
+void drop_graphs(sr_sb_ctx* c) {
+    for (auto& g : c->graph)
+        if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+}
+
+// w ping-pong parity of the context (a LOCAL group: of its slabs, which flip together)
+int group_wcur(sr_sb_ctx* c) { return c->backend == BK_LOCAL ? c->members[0]->wcur : c->wcur; }
+
+// Capture kGraphIters iterations (whole image: the 13-kernel iteration; slab mode: kernels, the
+// halo / all-to-all exchanges -- NCCL calls or the LOCAL device copies -- and the comm-stream
+// fork/join of the chunked transpose) into the graph of the current w parity.
 static sr_status build_graph(sr_sb_ctx* c) {
-    if (c->graph) { cudaGraphExecDestroy(c->graph); c->graph = nullptr; }
+    const int par = group_wcur(c);
+    if (c->graph[par]) { cudaGraphExecDestroy(c->graph[par]); c->graph[par] = nullptr; }
+    std::vector<sr_sb_ctx*> m = group_of(c);
+    std::vector<int> w0;
+    for (auto* x : m) w0.push_back(x->wcur);
     cudaGraph_t gr;
-    const int w0 = c->wcur;
     CK(cudaStreamBeginCapture(c->s, cudaStreamCaptureModeThreadLocal));
-    for (int i = 0; i < kGraphIters; i++) enq_iteration(c);
+    sr_status st = SR_OK;
+    for (int i = 0; i < kGraphIters && st == SR_OK; i++) st = c->slab ? slab_iteration(m) : enq_iteration(c);
     cudaError_t e = cudaStreamEndCapture(c->s, &gr);
-    c->wcur = w0;   // capture did not execute anything
+    for (size_t i = 0; i < m.size(); i++) m[i]->wcur = w0[i];   // capture did not execute anything
+    if (st != SR_OK) {
+        if (e == cudaSuccess) cudaGraphDestroy(gr);
+        return fail(c, st, m[0]->err);
+    }
     if (e != cudaSuccess) return fail(c, SR_ERR_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
-    e = cudaGraphInstantiate(&c->graph, gr, 0);
+    e = cudaGraphInstantiate(&c->graph[par], gr, 0);
     cudaGraphDestroy(gr);
-    if (e != cudaSuccess) { c->graph = nullptr; return fail(c, SR_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e)); }
-    c->graph_wcur = w0;
+    if (e != cudaSuccess) { c->graph[par] = nullptr; return fail(c, SR_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e)); }
     return SR_OK;
 }
 
@@ -1013,20 +1139,19 @@ sr_status sr_sb_iterate(sr_sb_ctx* c, int K) {
     if (K == 0) return SR_OK;
     DevGuard dg(c->device);
     RET(begin(c));
-    if (c->slab) {   // slab schedule: direct launches + exchanges (no graph)
-        std::vector<sr_sb_ctx*> m = group_of(c);
-        for (int i = 0; i < K; i++) {
-            sr_status st = slab_iteration(m);
-            if (st != SR_OK) return fail(c, st, m[0]->err);
-        }
-    } else {
-        int done = 0;
-        if (K >= kGraphIters) {
-            if (!c->graph || c->graph_wcur != c->wcur) RET(build_graph(c));
-            for (; done + kGraphIters <= K; done += kGraphIters) CK(cudaGraphLaunch(c->graph, c->s));
-            // the graph's w ping-pong flips are even, so wcur is unchanged
-        }
-        for (; done < K; done++) enq_iteration(c);
+    std::vector<sr_sb_ctx*> m = group_of(c);
+    const char* ev = std::getenv("SRSB_GRAPH");   // 0: direct launches only (A/B and debugging)
+    const bool use_graph = !(ev && ev[0] == '0');
+    int done = 0;
+    if (use_graph && K >= kGraphIters) {
+        const int par = group_wcur(c);
+        if (!c->graph[par]) RET(build_graph(c));
+        for (; done + kGraphIters <= K; done += kGraphIters) CK(cudaGraphLaunch(c->graph[par], c->s));
+        // the graph's w ping-pong flips are even, so the parity is unchanged
+    }
+    for (; done < K; done++) {
+        const sr_status st = c->slab ? slab_iteration(m) : enq_iteration(c);
+        if (st != SR_OK) return fail(c, st, m[0]->err);
     }
     RET(end(c));
     if (c->backend == BK_LOCAL)
@@ -1207,10 +1332,7 @@ sr_status sr_sb_set_monitor(sr_sb_ctx* c, int enable) {
     }
     c->sa.stats = c->stats;
     c->sa.stats_stride = c->stats_stride;
-    if (c->graph) {   // the captured graph bakes the kernel arguments: rebuild on the next iterate
-        cudaGraphExecDestroy(c->graph);
-        c->graph = nullptr;
-    }
+    drop_graphs(c);   // the captured graphs bake the kernel arguments: rebuild on the next iterate
     return SR_OK;
 }
 
@@ -1273,19 +1395,45 @@ void sr_sb_destroy(sr_sb_ctx* c) {
     for (auto* m : c->members) sr_sb_destroy(m);
     c->members.clear();
     if (c->comm) ncclCommDestroy(c->comm);
-    if (c->graph) cudaGraphExecDestroy(c->graph);
+    drop_graphs(c);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     void* ptrs[] = {c->phi_base, c->F_base, c->w_base[0], c->w_base[1], c->b_base, c->g_base, c->spec,
-                    c->spec_cols, c->twH, c->twM, c->twR, c->cM, c->cN, c->flag, c->stats, c->prev_phi, c->conv,
+                    c->spec_cols, c->twH, c->twM, c->twR, c->cM, c->cN, c->sym, c->flag, c->stats, c->prev_phi, c->conv,
                     c->aos_cpM, c->aos_rM, c->aos_cpN, c->aos_rN};
     for (void* q : ptrs)
         if (q) cudaFree(q);
     if (c->ev_in) cudaEventDestroy(c->ev_in);
     if (c->ev_out) cudaEventDestroy(c->ev_out);
+    for (cudaEvent_t e : c->xev)
+        if (e) cudaEventDestroy(e);
+    if (c->sc) cudaStreamDestroy(c->sc);
     if (c->s && c->own_stream) cudaStreamDestroy(c->s);
     delete c;
 }
 
 const char* sr_sb_last_error(const sr_sb_ctx* c) { return c ? c->err.c_str() : g_create_err.c_str(); }
+
+int sr_sb_slab_schedule(int kind, int P, int r, int Ml, int gh, int N, int k, int nk, long long* out, int max_ops) {
+    if (P < 1 || r < 0 || r >= P || Ml < 1 || gh < 1 || N < 2 || nk < 1 || k < 0 || k >= nk || kind < 0 || kind > 3)
+        return -1;
+    std::vector<XOp> ops;
+    if (kind <= 1) {
+        halo_ops(P, r, Ml, gh, N, kind == 0, 0, ops);
+    } else {
+        const long long blk = (long long)(N / 2 / P) * Ml;
+        if ((N / 2) % P || blk % nk) return -1;
+        a2a_ops(P, r, blk, k, nk, kind == 2, ops);
+    }
+    if (out) {
+        if ((int)ops.size() > max_ops) return -1;
+        for (size_t i = 0; i < ops.size(); i++) {
+            long long* q = out + 5 * i;
+            q[0] = ops[i].send; q[1] = ops[i].peer; q[2] = ops[i].buf; q[3] = ops[i].off; q[4] = ops[i].cnt;
+        }
+    }
+    return (int)ops.size();
+}
+
+int sr_sb_a2a_chunks(const sr_sb_ctx* c) { return c ? (c->backend == BK_LOCAL ? c->members[0]->a2a_chunks : c->a2a_chunks) : -1; }
 
 }  // extern "C"

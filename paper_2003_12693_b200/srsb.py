@@ -28,6 +28,7 @@ EXPORTS = ["sr_sb_default_params", "sr_sb_create", "sr_sb_set_image", "sr_sb_ite
            "sr_sb_last_error", "sr_sb_abi_version", "sr_sb_profile", "sr_sb_create_slab_group",
            "sr_sb_nccl_unique_id", "sr_sb_create_slab_nccl", "sr_sb_local_rows", "sr_sb_set_monitor",
            "sr_sb_get_monitor", "sr_sb_iterate_until", "sr_sb_last_change", "sr_sb_create_dist", "sr_sb_set_iteration",
+           "sr_sb_slab_schedule", "sr_sb_a2a_chunks",
            "sr_sb3_create", "sr_sb3_set_image", "sr_sb3_iterate", "sr_sb3_get_phi", "sr_sb3_get_state",
            "sr_sb3_set_state", "sr_sb3_debug_solve", "sr_sb3_debug_rhs", "sr_sb3_profile", "sr_sb3_sync",
            "sr_sb3_destroy", "sr_sb3_last_error"]
@@ -89,6 +90,8 @@ def lib():
             "sr_sb_last_change": (C.c_double, [p]),
             "sr_sb_create_dist": (st, [C.POINTER(Params), i, p, p, i, i, C.POINTER(p)]),
             "sr_sb_set_iteration": (st, [p, C.c_longlong]),
+            "sr_sb_slab_schedule": (i, [i, i, i, i, i, i, i, i, C.POINTER(C.c_longlong), i]),
+            "sr_sb_a2a_chunks": (i, [p]),
             "sr_sb3_create": (st, [C.POINTER(Params), i, i, p, C.POINTER(p)]),
             "sr_sb3_set_image": (st, [p, p, p]),
             "sr_sb3_iterate": (st, [p, i]),
@@ -117,6 +120,16 @@ def nccl_unique_id() -> bytes:
     if st != SR_OK:
         raise SrsbError(st, lib().sr_sb_last_error(None).decode())
     return buf.raw
+
+
+def slab_schedule(kind, P, r, Ml, gh, N, k=0, nk=1):
+    """sr_sb_slab_schedule: the exchange ops of slab r as a list of (send, peer, buf, off, cnt)."""
+    n = lib().sr_sb_slab_schedule(kind, P, r, Ml, gh, N, k, nk, None, 0)
+    if n < 0:
+        raise SrsbError(SR_ERR_ARG, "bad slab schedule arguments")
+    buf = (C.c_longlong * (5 * max(n, 1)))()
+    lib().sr_sb_slab_schedule(kind, P, r, Ml, gh, N, k, nk, buf, n)
+    return [tuple(int(buf[5 * i + j]) for j in range(5)) for i in range(n)]
 
 
 def default_params(M, N, batch=1, window=4) -> dict:
@@ -245,6 +258,11 @@ class Solver:
     @property
     def launches_per_iteration(self):
         return int(lib().sr_sb_launches_per_iteration(self._ctx))
+
+    @property
+    def a2a_chunks(self):
+        """Slab mode: spectrum all-to-all chunks pipelined with the column solve (1 = unchunked)."""
+        return int(lib().sr_sb_a2a_chunks(self._ctx))
 
     def profile(self, K):
         """sr_sb_profile: per kernel class {name: (ms_total, launches)} over K ungraphed iterations."""

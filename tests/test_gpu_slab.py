@@ -77,6 +77,34 @@ def test_slab_nccl_one_rank(S):
     assert np.array_equal(phi, ref_phi)
 
 
+@pytest.mark.parametrize("chunks,graph", [("1", "1"), ("2", "1"), ("4", "1"), ("4", "0"), ("8", "1")])
+def test_slab_chunked_alltoall_and_graph_bitwise(S, chunks, graph, monkeypatch):
+    """The pipelined transpose (all-to-all chunk k+1 on the comm stream while the column solve of
+    chunk k runs) and the CUDA graph of the slab iteration (kernels + exchanges +
+    fork/join) change no arithmetic: bitwise equal to the whole image, odd and even K."""
+    from synth import make_config
+    cfg = make_config("c5", size=(512, 512))
+    ref_phi, _ = _run(S, cfg, 5)
+    monkeypatch.setenv("SRSB_A2A_CHUNKS", chunks)
+    monkeypatch.setenv("SRSB_GRAPH", graph)
+    phi, _ = _run(S, cfg, 5, slabs=4)
+    assert np.array_equal(phi, ref_phi)
+    p = cfg["params"]
+    with S.Solver(512, 512, 1, window=p["window"], **{k: p[k] for k in KEYS}, slabs=4) as sv:
+        assert sv.a2a_chunks == int(chunks)
+
+
+def test_slab_nccl_one_rank_graph_and_chunks(S, monkeypatch):
+    """The NCCL backend's op lists (self pairs on a one-rank communicator) under the graph and the
+    chunked transpose: bitwise equal to the whole image."""
+    from synth import make_config
+    cfg = make_config("c5", size=(256, 256))
+    ref_phi, _ = _run(S, cfg, 4)
+    monkeypatch.setenv("SRSB_A2A_CHUNKS", "4")
+    phi, _ = _run(S, cfg, 4, nccl=(1, 0, S.nccl_unique_id()))
+    assert np.array_equal(phi, ref_phi)
+
+
 def test_slab_validation(S):
     from synth import make_config
     cfg = make_config("c1")

@@ -322,18 +322,33 @@ struct FftColArgs {
                         // (L2-resident, shared by the batch); null: sym_scale
 };
 
-// scale / symbol(k1, k2): from the table when the context has one, else the correctly rounded
-// reciprocal of the fp32 symbol
-__device__ __forceinline__ float sym_at(const FftColArgs& a, const float* __restrict__ cM, int M, int k1, int k2,
+// scale / symbol(k1, k2).  SYMT: from the table (staged into shared memory at the kernel start by
+// sym_stage, so its L2 latency hides behind the forward FFT); else the correctly rounded reciprocal of
+// the fp32 symbol.
+template <bool SYMT>
+__device__ __forceinline__ float sym_at(const FftColArgs& a, const float* __restrict__ cM, const float* st, int k1,
                                         float ck) {
-    return a.sym ? __ldg(&a.sym[(size_t)k2 * M + k1]) : sym_scale(a.scale, a.taumu, __ldg(&cM[k1]), ck);
+    if constexpr (SYMT) return st[k1];
+    else return sym_scale(a.scale, a.taumu, __ldg(&cM[k1]), ck);
 }
+// cp.async (4-byte, L1-bypassing where possible) of this thread's E table entries of column k2 into st
+template <int E, int T>
+__device__ __forceinline__ void sym_stage(const FftColArgs& a, int M, int k2, int t, float* st) {
+#pragma unroll
+    for (int u = 0; u < E; u++) {
+        const int k1 = t + u * T;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(st + k1)),
+                     "l"(a.sym + (size_t)k2 * M + k1) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void sym_wait() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // Column pass: forward FFT, divide by the symbol, inverse FFT, in place.  Threads of one column
 // are consecutive (t fastest), so a warp works inside one transform.
 // CONTIG: whole-image layout with G = 1 (one segment, each column M contiguous complex): element m
 // is col[m], so the E loads and stores use immediate offsets from one base pointer.
-template <int LOGM, int LOGE, bool CONTIG>
+template <int LOGM, int LOGE, bool CONTIG, bool SYMT>
 __global__ void __maxnreg__(LOGM >= 12 ? SRSB_COLS_MAXNREG_BIG : SRSB_COLS_MAXNREG) k_cols_solve(float2* __restrict__ spec, const float2* __restrict__ twM,
                                                        const float* __restrict__ cM, const float* __restrict__ cN,
                                                        FftColArgs a) {
@@ -348,6 +363,9 @@ __global__ void __maxnreg__(LOGM >= 12 ? SRSB_COLS_MAXNREG_BIG : SRSB_COLS_MAXNR
     const int kg = k2l >> a.lg_G, cc = k2l & (G - 1);
     float2* base = spec + b * a.bstride + cc;
     float2* sm = smem2 + cl * a.SC;
+    // SYMT: this column's scale / symbol entries, staged behind the exchange rows of the CTA's columns
+    float* st = reinterpret_cast<float*>(smem2 + (blockDim.x / T) * a.SC) + cl * M;
+    if constexpr (SYMT) sym_stage<E, T>(a, M, k2, t, st);
     // element m of the column (recomputed at the store: holding E 64-bit addresses across both FFTs
     // cost 32 registers)
     auto addr = [&](int m) -> long long {
@@ -365,6 +383,7 @@ __global__ void __maxnreg__(LOGM >= 12 ? SRSB_COLS_MAXNREG_BIG : SRSB_COLS_MAXNR
 #pragma unroll
     for (int u = 0; u < E; u++) v[u] = CONTIG ? col[t + u * T] : base[addr(t + u * T)];
     fft_stages<LOGM, LOGE, 0, false>(v, sm, t, twM);
+    if constexpr (SYMT) sym_wait();
     if (blockIdx.x == 0 && a.k2_off == 0) {  // CTA-uniform: slot 0 packs the real columns k2 = 0, N/2
 #pragma unroll
         for (int u = 0; u < E; u++) sm[pad16(t + u * T)] = v[u];
@@ -376,8 +395,8 @@ __global__ void __maxnreg__(LOGM >= 12 ? SRSB_COLS_MAXNREG_BIG : SRSB_COLS_MAXNR
                 const int k1 = t + u * T;
                 const float2 C = v[u];
                 const float2 Cc = conjf2(sm[pad16((M - k1) & (M - 1))]);
-                const float s0 = sym_at(a, cM, M, k1, 0, c0);
-                const float sh = sym_at(a, cM, M, k1, a.H, ch);
+                const float s0 = sym_at<SYMT>(a, cM, st, k1, c0);
+                const float sh = SYMT ? __ldg(&a.sym[(size_t)a.H * M + k1]) : sym_at<false>(a, cM, st, k1, ch);
                 const float p = 0.5f * (s0 + sh), m = 0.5f * (s0 - sh);
                 v[u] = make_float2(p * C.x + m * Cc.x, p * C.y + m * Cc.y);
             }
@@ -385,16 +404,16 @@ __global__ void __maxnreg__(LOGM >= 12 ? SRSB_COLS_MAXNREG_BIG : SRSB_COLS_MAXNR
             const float ck = __ldg(&cN[k2]);
 #pragma unroll
             for (int u = 0; u < E; u++) {
-                const float s = sym_at(a, cM, M, t + u * T, k2, ck);
+                const float s = sym_at<SYMT>(a, cM, st, t + u * T, ck);
                 v[u] = make_float2(v[u].x * s, v[u].y * s);
             }
         }
         __syncthreads();
     } else {
-        const float ck = __ldg(&cN[k2]);
+        const float ck = SYMT ? 0.f : __ldg(&cN[k2]);
 #pragma unroll
         for (int u = 0; u < E; u++) {
-            const float s = sym_at(a, cM, M, t + u * T, k2, ck);
+            const float s = sym_at<SYMT>(a, cM, st, t + u * T, ck);
             v[u] = make_float2(v[u].x * s, v[u].y * s);
         }
     }
@@ -412,7 +431,7 @@ __global__ void __maxnreg__(LOGM >= 12 ? SRSB_COLS_MAXNREG_BIG : SRSB_COLS_MAXNR
 // elected thread fetches the next column into a second shared buffer with a bulk async copy
 // (cp.async.bulk on an mbarrier) while the current one is transformed.  Same arithmetic as
 // k_cols_solve.
-template <int LOGM, int LOGE>
+template <int LOGM, int LOGE, bool SYMT>
 __global__ void __launch_bounds__(512, 1) k_cols_solve_p(float2* __restrict__ spec, const float2* __restrict__ twM,
                                                          const float* __restrict__ cM, const float* __restrict__ cN,
                                                          FftColArgs a, int ncols, int lg_hl) {
@@ -455,8 +474,8 @@ __global__ void __launch_bounds__(512, 1) k_cols_solve_p(float2* __restrict__ sp
                 const int k1 = t + u * T;
                 const float2 C = v[u];
                 const float2 Cc = conjf2(sm[pad16((M - k1) & (M - 1))]);
-                const float s0 = sym_at(a, cM, M, k1, 0, c0);
-                const float sh = sym_at(a, cM, M, k1, a.H, ch);
+                const float s0 = SYMT ? __ldg(&a.sym[k1]) : sym_at<false>(a, cM, nullptr, k1, c0);
+                const float sh = SYMT ? __ldg(&a.sym[(size_t)a.H * M + k1]) : sym_at<false>(a, cM, nullptr, k1, ch);
                 const float pp = 0.5f * (s0 + sh), mm = 0.5f * (s0 - sh);
                 v[u] = make_float2(pp * C.x + mm * Cc.x, pp * C.y + mm * Cc.y);
             }
@@ -465,7 +484,7 @@ __global__ void __launch_bounds__(512, 1) k_cols_solve_p(float2* __restrict__ sp
             const float ck = __ldg(&cN[k2]);
 #pragma unroll
             for (int u = 0; u < E; u++) {
-                const float sc = sym_at(a, cM, M, t + u * T, k2, ck);
+                const float sc = SYMT ? __ldg(&a.sym[(size_t)k2 * M + t + u * T]) : sym_at<false>(a, cM, nullptr, t + u * T, ck);
                 v[u] = make_float2(v[u].x * sc, v[u].y * sc);
             }
         }

@@ -73,6 +73,7 @@ struct sr_sb_ctx {
     float2 *twH = nullptr, *twM = nullptr, *twR = nullptr;
     float *cM = nullptr, *cN = nullptr;
     float* sym = nullptr;          // [H + 1][M] scale / symbol table (FftColArgs::sym), when small enough
+    bool use_sym = false;          // configure(): the column solve reads the table (SRSB_SYMTAB)
     int* flag = nullptr;
     int wcur = 0;
     long long k = 0;
@@ -205,7 +206,16 @@ sr_status configure(sr_sb_ctx* c) {
     const int lgH = ilog2(H), lgM = ilog2(M);
     c->rfwd = pick_row_fwd(lgH);
     c->rinv = pick_row_inv(lgH);
-    if (!c->rfwd || !c->rinv || !pick_col(lgM, false)) return fail(c, SR_ERR_SHAPE, "no FFT kernel for this size");
+    if (!c->rfwd || !c->rinv || !pick_col(lgM, false, false)) return fail(c, SR_ERR_SHAPE, "no FFT kernel for this size");
+    {   // scale / symbol table of the column solve (fp64-computed, rounded once; L2-resident, <= 16 MB).
+        // The column solve stages its column's entries into shared memory with cp.async at its start, so
+        // the L2 latency hides behind the forward FFT (C3: 0.149 ms per launch; the correctly rounded
+        // reciprocal of the fp32 symbol, SRSB_SYMTAB=0, also IEEE (Q20): 0.183 ms; round-1 table reads in
+        // the middle of the kernel: 0.189 ms).
+        const size_t nsym = (size_t)(H + 1) * M;
+        const char* ev = std::getenv("SRSB_SYMTAB");
+        c->use_sym = nsym <= ((size_t)4 << 20) && !(ev && ev[0] == '0');
+    }
     // Launch shapes (measured on B200, C3: smaller CTAs overlap load and FFT phases better):
     //  rows: rpc rows per CTA, 64..512 threads, <= ~72 KB shared;  E = min(16, H) values per thread
     const int E_h = H < 16 ? H : 16, T_h = H / E_h;
@@ -227,7 +237,7 @@ sr_status configure(sr_sb_ctx* c) {
         const int v = std::atoi(ev);
         if (v >= 1 && v <= H / P && (v & (v - 1)) == 0) G = v;
     }
-    c->cols = pick_col(lgM, !c->slab && G == 1);   // whole image, contiguous columns: immediate-offset access
+    c->cols = pick_col(lgM, !c->slab && G == 1, c->use_sym);   // whole image, contiguous columns: immediate-offset access
     c->rfwd = pick_row_fwd_shape(lgH, ilog2(rpc), ilog2(G));
     //  columns per CTA: >= 64 threads, <= 512 (a CTA may cover part of a column group)
     const int Hl = H / P;                            // spectrum columns this context solves
@@ -292,7 +302,7 @@ sr_status configure(sr_sb_ctx* c) {
     }
     {   // long contiguous columns (whole image, G = 1, M >= 4096): persistent prefetching solve
         const char* ev = std::getenv("SRSB_COLS_P");
-        c->cols_p = (!c->slab && G == 1 && !(ev && ev[0] == '0')) ? pick_col_p(lgM) : nullptr;
+        c->cols_p = (!c->slab && G == 1 && !(ev && ev[0] == '0')) ? pick_col_p(lgM, c->use_sym) : nullptr;
     }
     c->cgrid = dim3(Hl / cpc, B, 1);
     if (c->slab) {   // all-to-all chunks (column groups) pipelined with the column solve; SRSB_A2A_CHUNKS
@@ -303,7 +313,7 @@ sr_status configure(sr_sb_ctx* c) {
         c->a2a_chunks = std::max(nk, 1);
     }
     c->cblock = dim3(cpc * T_m, 1, 1);
-    c->csmem = cpc * c->ca.SC * (int)sizeof(float2);
+    c->csmem = cpc * c->ca.SC * (int)sizeof(float2) + (c->use_sym ? cpc * M * (int)sizeof(float) : 0);
     // stencils
     int smem = 0;
     bool ok = pick_stencil(p.window, p.window_shape, p.l == p.epsilon, c->rhs, c->wb, c->wb_mon, smem);
@@ -406,8 +416,10 @@ sr_status make_tables(sr_sb_ctx* c) {
     CK(cudaMemcpyAsync(c->twR, twR.data(), H * sizeof(float2), cudaMemcpyHostToDevice, c->s));
     CK(cudaMemcpyAsync(c->cM, cM.data(), M * sizeof(float), cudaMemcpyHostToDevice, c->s));
     CK(cudaMemcpyAsync(c->cN, cN.data(), (H + 1) * sizeof(float), cudaMemcpyHostToDevice, c->s));
-    if (c->sym) {   // scale / symbol(k1, k2) of Eq. (32) in fp64, rounded once to fp32 (Q10, Q20)
+    if (c->use_sym) {   // scale / symbol(k1, k2) of Eq. (32) in fp64, rounded once to fp32 (Q10, Q20)
         std::vector<float> sym((size_t)(H + 1) * M);
+        if (!c->sym && cudaMalloc((void**)&c->sym, sym.size() * sizeof(float)) != cudaSuccess)
+            return fail(c, SR_ERR_OOM, "symbol table allocation failed");
         const double tm = (double)c->p.tau * (double)c->p.mu, scale = 1.0 / ((double)M * (double)H);
         for (int k2 = 0; k2 <= H; k2++)
             for (int k1 = 0; k1 < M; k1++)
@@ -845,11 +857,6 @@ sr_status create_one(const sr_sb_params* p, int device, cudaStream_t stream, int
          alloc((void**)&c->cM, p->M * sizeof(float)) && alloc((void**)&c->cN, (p->N / 2 + 1) * sizeof(float)) &&
          alloc((void**)&c->flag, sizeof(int));
     if (ok && c->slab) ok = alloc((void**)&c->spec_cols, nspec * sizeof(float2));
-    {   // the symbol table when it stays L2-resident (<= 16 MB; SRSB_SYMTAB=0: the reciprocal path)
-        const size_t nsym = (size_t)(p->N / 2 + 1) * p->M;
-        const char* ev = std::getenv("SRSB_SYMTAB");
-        if (ok && nsym <= ((size_t)4 << 20) && !(ev && ev[0] == '0')) ok = alloc((void**)&c->sym, nsym * sizeof(float));
-    }
     if (ok && p->phi_solver == SR_PHI_AOS)
         ok = alloc((void**)&c->aos_cpM, p->M * 4) && alloc((void**)&c->aos_rM, p->M * 4) &&
              alloc((void**)&c->aos_cpN, p->N * 4) && alloc((void**)&c->aos_rN, p->N * 4);

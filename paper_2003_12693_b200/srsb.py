@@ -315,10 +315,14 @@ class DistSolver(Solver):
     Buffers hold this rank's rows [1][M/P][N]."""
 
     def __init__(self, M, N, window=4, device=None, stream=None, group=None, **params):
+        import torch
         import torch.distributed as tdist
         from .dist import broadcast_unique_id
         world, rank = tdist.get_world_size(group), tdist.get_rank(group)
-        ident = broadcast_unique_id(nccl_unique_id if rank == 0 else None, group=group, device=device)
+        # NCCL broadcasts device tensors only: resolve the device before the id exchange (gloo: CPU)
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else device)
+        bdev = dev if tdist.get_backend(group) == "nccl" else None
+        ident = broadcast_unique_id(nccl_unique_id if rank == 0 else None, group=group, device=bdev)
         super().__init__(M, N, 1, window=window, device=device, stream=stream, nccl=(world, rank, ident), **params)
 
 

@@ -116,3 +116,28 @@ def test_slab_validation(S):
     with pytest.raises(S.SrsbError):
         S.Solver(128, 128, 1, window=3, slabs=3)                 # not a power of two
     del p
+
+
+def test_dist_solver_on_one_rank_nccl_group(S):
+    """srsb.DistSolver with default arguments on an NCCL process group (the group bench.py uses): the
+    unique id is broadcast as a device tensor (NCCL has no CPU tensors), then the one-rank slab
+    context runs bitwise like the whole image."""
+    import socket
+    import torch.distributed as dist
+    from synth import make_config
+    cfg = make_config("c5", size=(256, 256))
+    ref_phi, _ = _run(S, cfg, 4)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", world_size=1, rank=0)
+    try:
+        p = cfg["params"]
+        with S.DistSolver(256, 256, window=p["window"], **{k: p[k] for k in KEYS}) as sv:
+            sv.set_image(torch.from_numpy(cfg["image"]).cuda(), torch.from_numpy(cfg["phi0"]).cuda())
+            sv.iterate(4)
+            phi = sv.get_phi().cpu().numpy()
+            sv.sync()
+    finally:
+        dist.destroy_process_group()
+    assert np.array_equal(phi, ref_phi)

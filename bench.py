@@ -31,7 +31,8 @@ METRIC = "megapixel-iterations/s per SB-SR iteration"
 UNIT = "Mpx-iter/s"
 # algorithmic HBM bytes per pixel per launch of each kernel class
 BYTES_PER_PX = {"rhs": 28.0, "rows_r2c": 8.0, "cols_solve": 8.0, "rows_c2r": 12.0, "wb": 40.0,
-                "aos_vert": 8.0, "aos_horiz": 12.0}   # aos_vert: register-chunk kernel (M <= 2048)
+                "aos_vert": 8.0, "aos_horiz": 12.0,   # aos_vert: register-chunk kernel (M <= 2048)
+                "rhs_r2c": 28.0}   # fused RHS + row R2C: phi, w1, w2, b1, b2, g in, packed half spectrum out
 MODEL_BYTES_PER_PX_ITER = 172.0   # SURVEY.md §8(d) fused model (S = 3)
 
 
@@ -153,11 +154,24 @@ def cpu_baseline_oracle(cfg, target_s=12.0):
                       f"OMP_NUM_THREADS={os.environ.get('OMP_NUM_THREADS')}, {t:.1f} s"}
 
 
-def cufft_reference(nb, M, N, dev, stream, kernels, reps=5):
+def cufft_reference(nb, M, N, dev, stream, kernels, reps=5, solver_factory=None):
     """cuFFT R2C + C2R (torch.fft, i.e. cuFFT) on the same batch of M x N fp32 fields,
     timed next to our three-pass solve (k_rows_r2c + k_cols_solve + k_rows_c2r, which also applies
-    the symbol and the increment).  Never on the hot path; measured after the timed regions."""
+    the symbol and the increment).  Never on the hot path; measured after the timed regions.  When the
+    measured context fuses the row R2C into the RHS kernel, the three passes are profiled on a second,
+    unfused context (SRSB_FUSE=0) of the same shape (solver_factory)."""
     import torch
+    if "rows_r2c" not in kernels and solver_factory is not None:
+        os.environ["SRSB_FUSE"] = "0"
+        try:
+            sv2, img, phi0 = solver_factory()
+            sv2.set_image(img, phi0)
+            prof = sv2.profile(1)
+            sv2.sync()
+            sv2.close()
+        finally:
+            del os.environ["SRSB_FUSE"]
+        kernels = {k: {"ms_per_launch": v[0] / v[1]} for k, v in prof.items()}
     x = torch.randn(nb, M, N, device=dev, dtype=torch.float32)
     with torch.cuda.stream(stream):
         for _ in range(2):
@@ -502,7 +516,10 @@ def main():
     launches = args.steps * (4 + K * sv.launches_per_iteration)
     fft_ref = None
     if rank == 0 and mode != "slab" and not args.no_fft_ref and "kernels" in roofline:
-        fft_ref = cufft_reference(nb, M, N, dev, stream, roofline["kernels"])
+        def factory():
+            return (Solver(M, N, nb, window=p["window"], device=local, stream=stream, phi_solver=cfg["phi_solver"],
+                           **{k: p[k] for k in keys}), img_d, phi0_d)
+        fft_ref = cufft_reference(nb, M, N, dev, stream, roofline["kernels"], solver_factory=factory)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline_oracle(cfg)

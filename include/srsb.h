@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define SRSB_ABI_VERSION 1
+#define SRSB_ABI_VERSION 2   /* 2: SR_K_RHS_R2C (SR_K_NCLASSES 7 -> 8) */
 
 typedef enum {
     SR_OK = 0,
@@ -173,7 +173,9 @@ sr_status sr_sb_debug_wb(sr_sb_ctx* ctx);
 /* Kernel classes of the hot path, in launch order within a sweep / iteration. */
 typedef enum { SR_K_RHS = 0, SR_K_ROWS_R2C = 1, SR_K_COLS_SOLVE = 2, SR_K_ROWS_C2R = 3, SR_K_WB = 4,
                SR_K_AOS_VERT = 5, SR_K_AOS_HORIZ = 6,   /* phi_solver = SR_PHI_AOS replaces classes 1-3 */
-               SR_K_NCLASSES = 7 } sr_kernel_class;
+               SR_K_RHS_R2C = 7,   /* the fused RHS (Eq. 37) + row R2C cluster kernel: replaces classes 0-1 for
+                                      whole-image FFT contexts with 128 <= N <= 1024 */
+               SR_K_NCLASSES = 8 } sr_kernel_class;
 
 /* Diagnostics: run K outer iterations WITHOUT the CUDA graph, bracketing every launch with CUDA
  * events on the context's work stream, and return per kernel class (sr_kernel_class) the summed

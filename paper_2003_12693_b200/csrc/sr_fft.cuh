@@ -124,10 +124,18 @@ __device__ __forceinline__ void dft_reg(float2 (&x)[R]) {
     for (int k = 0; k < R; k++) x[k] = y[k];
 }
 
+// CTA barrier of the FFT stages: NBAR = 0 -> __syncthreads(); NBAR > 0 -> named barrier 1 over the
+// first NBAR threads (a subset of the CTA runs the transforms: k_rhs_r2c)
+template <int NBAR>
+__device__ __forceinline__ void fft_bar() {
+    if constexpr (NBAR == 0) __syncthreads();
+    else asm volatile("bar.sync 1, %0;" ::"n"(NBAR) : "memory");
+}
+
 // Stockham stages of an N-point FFT (N = 2^LOGN) by T = N/E threads, thread t.
 // On entry of the first stage v[u] = x[t + u T]; on exit v[u] = X[t + u T].
 // sm: this transform's padded float2 shared-memory row.  tw[m] = exp(-2 pi i m / N).
-template <int LOGN, int LOGE, int LOGNS, bool INV>
+template <int LOGN, int LOGE, int LOGNS, bool INV, int NBAR = 0>
 __device__ __forceinline__ void fft_stages(float2 (&v)[1 << LOGE], float2* __restrict__ sm, int t,
                                            const float2* __restrict__ tw) {
     constexpr int N = 1 << LOGN, E = 1 << LOGE, T = N / E;
@@ -139,7 +147,7 @@ __device__ __forceinline__ void fft_stages(float2 (&v)[1 << LOGE], float2* __res
         for (int q = 0; q < Q; q++)
 #pragma unroll
             for (int r = 0; r < R; r++) v[q + r * Q] = sm[pad16(t + q * T + r * (N / R))];
-        __syncthreads();
+        fft_bar<NBAR>();
     }
 #pragma unroll
     for (int q = 0; q < Q; q++) {
@@ -180,8 +188,8 @@ __device__ __forceinline__ void fft_stages(float2 (&v)[1 << LOGE], float2* __res
         }
     }
     if constexpr (!LAST) {
-        __syncthreads();
-        fft_stages<LOGN, LOGE, LOGNS + LOGR, INV>(v, sm, t, tw);
+        fft_bar<NBAR>();
+        fft_stages<LOGN, LOGE, LOGNS + LOGR, INV, NBAR>(v, sm, t, tw);
     }
 }
 

@@ -3,6 +3,7 @@
 #pragma once
 #include "sr_fft.cuh"
 #include "sr_stencil.cuh"
+#include "sr_fused.cuh"
 
 namespace srsb {
 
@@ -12,6 +13,7 @@ typedef void (*ColKernel)(float2*, const float2*, const float*, const float*, Ff
 typedef void (*RhsKernel)(const float*, const float*, const float*, const float*, float*, StencilArgs);
 typedef void (*RhsTmaKernel)(const RhsMaps, const float*, float*, StencilArgs);
 typedef void (*WbTmaKernel)(const RhsMaps, float*, float*, int*, StencilArgs);
+typedef void (*RhsR2cKernel)(const RhsMaps, const float*, float2*, const float2*, const float2*, StencilArgs, int);
 typedef void (*WbKernel)(const float*, const float*, float*, float*, const float*, int*, StencilArgs);
 
 RowKernel pick_row_fwd(int log2_h);       // fft_r2c.cu
@@ -27,7 +29,11 @@ bool pick_stencil(int R, int shape, bool leq, RhsKernel& rhs, WbKernel (&wb)[2][
 bool pick_tma(int R, int shape, bool leq, RhsTmaKernel& k, WbTmaKernel (&wb)[2][2], WbTmaKernel& wb_mon,
               int& smem_rhs, int& smem_wb);
 
-#define SRSB_DECLARE_STENCIL(R) bool pick_stencil_r##R(int shape, bool leq, RhsKernel& rhs, WbKernel (&wb)[2][2], WbKernel& wb_mon, int& smem); \
+// k_rhs_r2c (sr_fused.cuh) for N = 2^(log2_h + 1) in 128 .. 1024; null if not instantiated
+RhsR2cKernel pick_fused(int R, int shape, bool leq, int log2_h, int& smem);
+
+#define SRSB_DECLARE_STENCIL(R) RhsR2cKernel pick_fused_r##R(int shape, bool leq, int log2_h, int& smem); \
+ bool pick_stencil_r##R(int shape, bool leq, RhsKernel& rhs, WbKernel (&wb)[2][2], WbKernel& wb_mon, int& smem); \
     bool pick_tma_r##R(int shape, bool leq, RhsTmaKernel& k, WbTmaKernel (&wb)[2][2], WbTmaKernel& wb_mon, int& smem_rhs, int& smem_wb);
 SRSB_DECLARE_STENCIL(0) SRSB_DECLARE_STENCIL(1) SRSB_DECLARE_STENCIL(2) SRSB_DECLARE_STENCIL(3)
 SRSB_DECLARE_STENCIL(4) SRSB_DECLARE_STENCIL(5) SRSB_DECLARE_STENCIL(6) SRSB_DECLARE_STENCIL(7)

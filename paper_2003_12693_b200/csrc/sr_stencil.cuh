@@ -203,6 +203,7 @@ struct StencilArgs {
     int tiles_x, tiles_y, ntiles;   // tiles per row, per column, total (x batch)
     int gh;            // ghost rows above each plane (TMA coordinates address the allocation rows)
     int aos;           // 1: emit the full RHS F (AOS phi solver, NEXT-4); 0: the increment D = F - A psi
+    int band_skip;     // 1: window sums only in the narrow band (exact, needs_v); 0: everywhere (SRSB_BAND_SKIP=0)
     double* stats;     // NEXT-1 monitor: per image [E_g, E_a, E_r, E_pen, ...] accumulated by k_wb; null = off
     int stats_stride;  // doubles per image in stats
 };
@@ -680,6 +681,38 @@ struct TmaGeom {
     static constexpr uint32_t TX1 = (uint32_t)(3 * PW * PH) * 4, TX2 = (uint32_t)(2 * BW * BH + TW * TH) * 4;
 };
 
+// Narrow band (Eq. 11 and 28).  Every use of the window sum v is multiplied by
+// h(psi) (w/b update, Eq. 41) or h'(psi) (RHS, Eq. 37), which are EXACTLY zero where the regularizer
+// functions take their early exit: |psi| / eps >= 2 (l = eps) or |psi| >= l + eps and |psi| > eps.
+// needs_v is the negation of that exit test (same fp32 expressions), so skipping the window sums (and
+// the u staging of a tile none of whose pixels needs v) changes no result: the skipped terms are
+// 0 * finite.  Out of the band -- most pixels, since the band follows the contour -- a stencil tile is
+// then the pointwise part and its loads only.
+template <bool LEQ>
+__device__ __forceinline__ bool needs_v(float x, const Reg& r) {
+    if constexpr (LEQ) return !(fabsf(x * r.inv_eps) >= 2.f);
+    else return !(fabsf(x) >= r.l + r.eps && fabsf(x) > r.eps);
+}
+// any of the thread's RT x 2 tile pixels (rows inside the image) in the band; Ps = the phi box
+template <bool LEQ, class G>
+__device__ __forceinline__ bool block_needs_v(const float* Ps, int r0, int c0, int row0, int M, const Reg& r) {
+    bool need = false;
+#pragma unroll
+    for (int i = 0; i < G::RT; i++) {
+        if (row0 + r0 + i >= M) break;
+        const float2 P = *reinterpret_cast<const float2*>(Ps + (G::HR + r0 + i) * G::PW + G::CA + c0);
+        need |= needs_v<LEQ>(P.x, r) || needs_v<LEQ>(P.y, r);
+    }
+    return need;
+}
+template <int RT>
+__device__ __forceinline__ void zero_v(float2 (&v)[RT][ST_CT]) {
+#pragma unroll
+    for (int i = 0; i < RT; i++)
+#pragma unroll
+        for (int c = 0; c < ST_CT; c++) v[i][c] = make_float2(0.f, 0.f);
+}
+
 // u = h(phi) w over the tile + R halo from the group-1 boxes, as 16-byte chunks (2 px x 2 channels)
 // in TileGeom's layout; rows outside the image give u = 0 (reading Q5).  Branch-free, f32x2.
 #ifndef SRSB_STAGE_U_OLD
@@ -718,11 +751,13 @@ __device__ __forceinline__ void stage_u_tma(float4* __restrict__ U, const float*
 // The pointwise part of Eq. (37) (increment form) for the thread's RT x 2 block,
 // both pixels of a row in f32x2.  EDGE = false: the tile touches no image boundary (no masks, no
 // periodic wrap loads, no ragged rows).
-template <int R, bool LEQ, bool EDGE, class G>
+// TOREG: the results go to res[i] (k_rhs_r2c keeps the tile of D on chip) instead of D in global memory.
+template <int R, bool LEQ, bool EDGE, class G, bool TOREG = false>
 __device__ __forceinline__ void rhs_points_tma(const float* Ps, const float* W1s, const float* W2s, const float* B1s,
                                                const float* B2s, const float* Gs, const float* __restrict__ phi,
                                                float* __restrict__ D, const float2 (&v)[G::RT][ST_CT], int img,
-                                               int row0, int r0, int c0, int col0, const StencilArgs& a) {
+                                               int row0, int r0, int c0, int col0, const StencilArgs& a,
+                                               float2* res = nullptr) {
     const int M = a.M, N = a.N, gj = col0 + c0;
     const float* ph = phi + img * a.plane;
     float* Do = D + img * a.plane;
@@ -779,7 +814,8 @@ __device__ __forceinline__ void rhs_points_tma(const float* Ps, const float* W1s
         t = fma2(f2(2.f * a.beta), mul2(hp, wv), t);
         t = fma2(f2(a.mu), dv, t);
         const float2 out = a.aos ? fma2(f2(a.tau), t, P) : mul2(f2(a.tau), fma2(f2(a.mu), lap, t));
-        *reinterpret_cast<float2*>(Do + (long long)gi * N + gj) = out;
+        if constexpr (TOREG) res[i] = out;
+        else *reinterpret_cast<float2*>(Do + (long long)gi * N + gj) = out;
         Pc = P;
         P = Pn;
         c1c = c1n;
@@ -859,14 +895,19 @@ __global__ void __launch_bounds__(256, SRSB_TMA_MINB) k_rhs_tma(const __grid_con
         }
     }
     mbar_wait(&bar[0], 0);
-    // u = h(phi) w over the tile + R halo, as 16-byte chunks (2 px x 2 channels) in TileGeom's layout
-    stage_u_tma<R, LEQ, G>(U, Ps, W1s, W2s, row0, tid, a);
-    __syncthreads();
     const int r0 = threadIdx.y * G::RT, c0 = threadIdx.x * ST_CT;
     const int M = a.M, N = a.N, gj = col0 + c0;
     const bool active = gj < N && row0 + r0 < M;
+    // narrow band: v only where h'(psi) != 0; u staged only if some pixel of the tile needs v
+    const bool own = !a.band_skip || (active && block_needs_v<LEQ, G>(Ps, r0, c0, row0, M, a.reg));
     float2 v[G::RT][ST_CT];
-    if (active) window_block<R, SHAPE, G::RT, G::LDC>(U, r0, c0, a.e, v);
+    zero_v<G::RT>(v);
+    if (__syncthreads_or(own)) {
+        // u = h(phi) w over the tile + R halo, as 16-byte chunks (2 px x 2 channels) in TileGeom's layout
+        stage_u_tma<R, LEQ, G>(U, Ps, W1s, W2s, row0, tid, a);
+        __syncthreads();
+        if (active && own) window_block<R, SHAPE, G::RT, G::LDC>(U, r0, c0, a.e, v);
+    }
     __syncthreads();   // u is dead: group 2 lands in its place
     if (tid == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic reads of u before async writes
@@ -948,13 +989,18 @@ __global__ void __launch_bounds__(256, SRSB_TMA_MINB) k_wb_tma(const __grid_cons
         }
     }
     mbar_wait(&bar[0], 0);
-    stage_u_tma<R, LEQ, G>(U, Ps, W1s, W2s, row0, tid, a);
-    __syncthreads();
     const int r0 = threadIdx.y * G::RT, c0 = threadIdx.x * ST_CT;
     const int M = a.M, N = a.N, gj = col0 + c0;
     const bool active = gj < N && row0 + r0 < M;
+    // narrow band: v' only where h(phi^{k+1}) != 0 (Eq. 41; the monitor's E_r carries the same factor)
+    const bool own = !a.band_skip || (active && block_needs_v<LEQ, G>(Ps, r0, c0, row0, M, a.reg));
     float2 v[G::RT][ST_CT];
-    if (active) window_block<R, SHAPE, G::RT, G::LDC>(U, r0, c0, a.e, v);
+    zero_v<G::RT>(v);
+    if (__syncthreads_or(own)) {
+        stage_u_tma<R, LEQ, G>(U, Ps, W1s, W2s, row0, tid, a);
+        __syncthreads();
+        if (active && own) window_block<R, SHAPE, G::RT, G::LDC>(U, r0, c0, a.e, v);
+    }
     __syncthreads();   // u is dead: group 2 lands in its place
     if (tid == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

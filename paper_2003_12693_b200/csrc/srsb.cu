@@ -93,6 +93,8 @@ struct sr_sb_ctx {
     RhsMaps tmaps[2];                 // tensor maps, per w ping-pong buffer
     dim3 tgrid;
     int tsmem = 0, tsmem_wb = 0;
+    RhsR2cKernel rhs_r2c = nullptr;   // fused RHS + row R2C cluster kernel (whole image, FFT solve, 128 <= N <= 1024)
+    int fsmem = 0, fsr = 0, fnct = 0;  // its shared bytes, FFT row stride (float2), cluster size (CTAs per band)
     WbKernel wb[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
     WbKernel wb_mon = nullptr;     // monitor variant (threshold mode, last pass)
     FftRowArgs ra{};
@@ -347,6 +349,10 @@ sr_status configure(sr_sb_ctx* c) {
     a.w_proj = p.w_proj;
     a.b_max = p.b_max;
     a.aos = p.phi_solver == SR_PHI_AOS ? 1 : 0;
+    {
+        const char* e = getenv("SRSB_BAND_SKIP");
+        a.band_skip = (e && e[0] == '0') ? 0 : 1;
+    }
     a.gh = c->gh;
     {   // TMA-staged RHS
         const char* e = getenv("SRSB_TMA");
@@ -374,6 +380,42 @@ sr_status configure(sr_sb_ctx* c) {
                                     c->tsmem_wb));
         } else {
             c->rhs_tma = nullptr;
+        }
+    }
+    {   // fused RHS + row R2C (sr_fused.cuh): one cluster per 32-row band, N / 64 CTAs.  Opt-in (SRSB_FUSE=1):
+        // measured 2x slower than k_rhs_tma + k_rows_r2c on C3 (1.11 vs 0.555 ms per sweep): 16-CTA clusters
+        // reach 21 active clusters (76 % of the CTA slots) and stall on the cluster barriers
+        const char* e = getenv("SRSB_FUSE");
+        c->rhs_r2c = nullptr;
+        if (c->rhs_tma && !c->slab && p.phi_solver == SR_PHI_FFT && G == 1 && N >= 128 && N <= 1024 &&
+            e && e[0] == '1') {
+            int fs = 0;
+            RhsR2cKernel k = pick_fused(p.window, p.window_shape, p.l == p.epsilon, lgH, fs);
+            const int nct = N / ST_TW, rows = TMA_TH / nct;
+            if (k) {
+                CK(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, fs));
+                if (nct > 8) CK(cudaFuncSetAttribute((const void*)k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+                cudaLaunchConfig_t cfg = {};
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeClusterDimension;
+                at[0].val.clusterDim.x = nct;
+                at[0].val.clusterDim.y = 1;
+                at[0].val.clusterDim.z = 1;
+                cfg.gridDim = c->tgrid;
+                cfg.blockDim = c->sblock;
+                cfg.dynamicSmemBytes = fs;
+                cfg.attrs = at;
+                cfg.numAttrs = 1;
+                int ncl = 0;
+                if (cudaOccupancyMaxActiveClusters(&ncl, (const void*)k, &cfg) == cudaSuccess && ncl > 0) {
+                    c->rhs_r2c = k;
+                    c->fsmem = fs;
+                    c->fnct = nct;
+                    c->fsr = padded(H, rows >= 16 ? 1 : (16 / rows) & 15);
+                } else {
+                    cudaGetLastError();
+                }
+            }
         }
     }
     // opt-in shared memory above 48 KB
@@ -516,6 +558,25 @@ void enq_rhs(sr_sb_ctx* c, float* F) {
     else
         c->rhs<<<c->sgrid, c->sblock, c->ssmem, c->s>>>(c->phi, c->w[c->wcur], c->b, c->g, F, c->sa);
     prof_end(c, SR_K_RHS);
+}
+// fused RHS + row R2C: D of Eq. (37) (increment form) straight into the transposed half spectrum
+void enq_rhs_r2c(sr_sb_ctx* c) {
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = c->fnct;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = c->tgrid;
+    cfg.blockDim = c->sblock;
+    cfg.dynamicSmemBytes = c->fsmem;
+    cfg.stream = c->s;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    prof_begin(c);
+    cudaLaunchKernelEx(&cfg, c->rhs_r2c, (const RhsMaps)c->tmaps[c->wcur], (const float*)c->phi, c->spec,
+                       (const float2*)c->twH, (const float2*)c->twR, c->sa, c->fsr);
+    prof_end(c, SR_K_RHS_R2C);
 }
 void enq_wb_pass(sr_sb_ctx* c, int last) {
     prof_begin(c);
@@ -699,8 +760,14 @@ void enq_aos(sr_sb_ctx* c, const float* F, float* out, float clip) {
 sr_status enq_iteration(sr_sb_ctx* c) {   // whole-image context
     if (c->stats) cudaMemsetAsync(c->stats, 0, sizeof(double) * c->stats_stride * c->p.batch, c->s);
     for (int s = 0; s < c->p.S; s++) {
-        enq_rhs(c, c->F);
         const float clip = (s == c->p.S - 1) ? c->p.phi_clip : 0.f;
+        if (c->rhs_r2c) {
+            enq_rhs_r2c(c);
+            enq_cols(c);
+            enq_c2r(c, c->phi, clip, 1, s);
+            continue;
+        }
+        enq_rhs(c, c->F);
         if (c->p.phi_solver == SR_PHI_AOS) {
             enq_aos(c, c->F, c->phi, clip);
         } else {
@@ -1390,7 +1457,8 @@ double sr_sb_last_change(const sr_sb_ctx* c) { return c ? c->last_change : -1.0;
 
 int sr_sb_launches_per_iteration(const sr_sb_ctx* c) {
     if (!c) return -1;
-    const int per_sweep = c->p.phi_solver == SR_PHI_AOS ? 3 : 4;   // rhs + (r2c, cols, c2r | vert, horiz)
+    // rhs + (r2c, cols, c2r | vert, horiz); fused: rhs_r2c, cols, c2r
+    const int per_sweep = (c->p.phi_solver == SR_PHI_AOS || c->rhs_r2c) ? 3 : 4;
     const int per = per_sweep * c->p.S + (c->p.w_mode == SR_W_FIXED_POINT ? c->p.w_iters : 1);
     return c->backend == BK_LOCAL ? per * (int)c->members.size() : per;
 }

@@ -42,4 +42,20 @@ bool SRSB_CAT(pick_tma_r, SRSB_R)(int shape, bool leq, RhsTmaKernel& k, WbTmaKer
     smem_wb = WbGeom<SRSB_R>::BYTES;
     return true;
 }
+template <int SH, bool LEQ>
+static RhsR2cKernel fused_h(int log2_h) {
+    switch (log2_h) {
+        case 6: return k_rhs_r2c<SRSB_R, SH, LEQ, 6>;
+        case 7: return k_rhs_r2c<SRSB_R, SH, LEQ, 7>;
+        case 8: return k_rhs_r2c<SRSB_R, SH, LEQ, 8>;
+        case 9: return k_rhs_r2c<SRSB_R, SH, LEQ, 9>;
+    }
+    return nullptr;
+}
+RhsR2cKernel SRSB_CAT(pick_fused_r, SRSB_R)(int shape, bool leq, int log2_h, int& smem) {
+    smem = TmaGeom<SRSB_R>::BYTES;
+    if (shape == 0) return leq ? fused_h<0, true>(log2_h) : fused_h<0, false>(log2_h);
+    if (shape == 1) return leq ? fused_h<1, true>(log2_h) : fused_h<1, false>(log2_h);
+    return nullptr;
+}
 }  // namespace srsb

@@ -15,6 +15,20 @@ bool pick_stencil(int R, int shape, bool leq, RhsKernel& rhs, WbKernel (&wb)[2][
     }
     return false;
 }
+RhsR2cKernel pick_fused(int R, int shape, bool leq, int log2_h, int& smem) {
+    switch (R) {
+        case 0: return pick_fused_r0(shape, leq, log2_h, smem);
+        case 1: return pick_fused_r1(shape, leq, log2_h, smem);
+        case 2: return pick_fused_r2(shape, leq, log2_h, smem);
+        case 3: return pick_fused_r3(shape, leq, log2_h, smem);
+        case 4: return pick_fused_r4(shape, leq, log2_h, smem);
+        case 5: return pick_fused_r5(shape, leq, log2_h, smem);
+        case 6: return pick_fused_r6(shape, leq, log2_h, smem);
+        case 7: return pick_fused_r7(shape, leq, log2_h, smem);
+        case 8: return pick_fused_r8(shape, leq, log2_h, smem);
+    }
+    return nullptr;
+}
 bool pick_tma(int R, int shape, bool leq, RhsTmaKernel& k, WbTmaKernel (&wb)[2][2], WbTmaKernel& wb_mon,
               int& smem_rhs, int& smem_wb) {
     switch (R) {

@@ -474,3 +474,29 @@ def test_launch_shape_instances_bitwise(S, M, N, env, monkeypatch):
     with _solver(S, M, N, 2, p) as sv:
         out = _np(sv.debug_solve(_cuda(F)))
     assert np.array_equal(out, ref)
+
+
+@pytest.mark.parametrize("name,size,K", [("c1", None, 20), ("c3", (1024, 1024), 6), ("c4", (512, 512), 6),
+                                         ("c2", None, 8)])
+def test_band_skip_is_exact(S, monkeypatch, name, size, K):
+    """The narrow-band skip of the window sums (sr_stencil.cuh needs_v) drops only terms
+    that are multiplied by an exact zero (h or h' off the band): trajectories with and without it are
+    bitwise equal, on configs where most tiles lie off the band."""
+    from synth import make_config
+    cfg = make_config(name, size=size) if name != "c3" else make_config("c3", images=[0, 1])
+    p = cfg["params"]
+    B, M, N = cfg["image"].shape
+
+    def run():
+        with _solver(S, M, N, B, p) as sv:
+            sv.set_image(_cuda(cfg["image"]), _cuda(cfg["phi0"]))
+            sv.iterate(K)
+            st = sv.get_state()
+            out = {k: v.cpu().numpy() for k, v in st.items()}
+            sv.sync()
+        return out
+    a = run()
+    monkeypatch.setenv("SRSB_BAND_SKIP", "0")
+    b = run()
+    for k in ("phi", "w", "b"):
+        assert np.array_equal(a[k], b[k]), k

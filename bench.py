@@ -125,33 +125,48 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def cpu_baseline_oracle(cfg, target_s=12.0):
+def cpu_model() -> str:
+    """The host CPU's model name (/proc/cpuinfo), for the cpu_baseline record."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline_oracle(cfg, target_s=20.0):
     """The float64 oracle as it stands, on this host's cores, on a bounded sample of the workload:
-    one image of the config, as many iterations as fit ~target_s (at least 1)."""
+    for C3 four images spread over the batch (0, 21, 42, 63), for the single-image configs the image;
+    the same number of iterations on each, as many as fit ~target_s in total (at least 1)."""
     import numpy as np
     import oracle
     from synth import make_config
     cores = len(os.sched_getaffinity(0))
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
-    c = make_config(cfg["name"], images=[0]) if cfg["name"] == "c3" else make_config(cfg["name"])
+    imgs = [0, 21, 42, 63] if cfg["name"] == "c3" else [None]
+    c = make_config(cfg["name"], images=imgs) if cfg["name"] == "c3" else make_config(cfg["name"])
     p = dict(c["params"], phi_solver=cfg["phi_solver"])
-    img, phi0 = c["image"][0], c["phi0"][0]
-    M, N = img.shape
-    g = oracle.edge(img, p["sigma"], p["rho"], p["s"])
-    st = oracle.init(phi0)
+    M, N = c["image"].shape[1:]
+    states = []
+    for b in range(len(imgs)):
+        g = oracle.edge(c["image"][b], p["sigma"], p["rho"], p["s"])
+        states.append((oracle.init(c["phi0"][b]), g))
     t0 = time.perf_counter()
-    oracle.iterate(p, st, g, 1)
+    oracle.iterate(p, states[0][0], states[0][1], 1)
     t1 = time.perf_counter() - t0
-    k = max(1, int(target_s / max(t1, 1e-3)) - 1)
+    k = max(1, int(target_s / len(imgs) / max(t1, 1e-3)))
     t0 = time.perf_counter()
-    oracle.iterate(p, st, g, k)
-    t = time.perf_counter() - t0
-    k += 1
-    t += t1
+    for b, (st, g) in enumerate(states):
+        oracle.iterate(p, st, g, k - 1 if b == 0 else k)
+    t = time.perf_counter() - t0 + t1
     del np
-    return {"value": M * N * k / t / 1e6, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"1 image of {cfg['name']} ({M}x{N}), {k} SB iterations, float64 C oracle, "
-                      f"OMP_NUM_THREADS={os.environ.get('OMP_NUM_THREADS')}, {t:.1f} s"}
+    return {"value": len(imgs) * M * N * k / t / 1e6, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "cpu_model": cpu_model(),
+            "sample": f"{len(imgs)} image(s) of {cfg['name']} ({M}x{N}"
+                      f"{', images ' + str(imgs) if imgs[0] is not None else ''}), {k} SB iterations each, "
+                      f"float64 C oracle, OMP_NUM_THREADS={os.environ.get('OMP_NUM_THREADS')}, {t:.1f} s"}
 
 
 def cufft_reference(nb, M, N, dev, stream, kernels, reps=5, solver_factory=None):
@@ -217,7 +232,7 @@ def run_reference(args, cfg, rank):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": config_json(cfg, args.gpus),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
                              "sample": f"each step = 1 SB iteration of image 0 of {cfg['name']} ({M}x{N}), "
                                        f"float64 C oracle, OMP_NUM_THREADS={os.environ['OMP_NUM_THREADS']}"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

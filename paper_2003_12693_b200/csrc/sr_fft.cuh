@@ -21,6 +21,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include "sr_tma.cuh"
+#include "sr_reduce.cuh"
 
 namespace srsb {
 
@@ -201,7 +202,8 @@ struct FftRowArgs {
     int SR;         // float2 per shared row, padded
     float clip;     // c2r only: > 0 clamps the output to [-clip, clip]
     int accum;      // c2r only: 1 -> phi = phi + z (increment form), 0 -> phi = z
-    double* stats;  // c2r monitor: per image [.., sum (phi_new - phi_old)^2, sum phi_old^2] at `stats` (null = off)
+    double* stats;  // c2r monitor: per-CTA partials [image][CTA][sum (phi_new - phi_old)^2, sum phi_old^2]
+                    // of this sweep (null = off); k_reduce_partials sums them per image
     int stats_stride;
 };
 
@@ -504,16 +506,32 @@ __global__ void __launch_bounds__(512, 1) k_cols_solve_p(float2* __restrict__ sp
     }
 }
 
+// NEXT-1 monitor partials of the c2r pass, out of line so the (untaken, monitor-off) branch costs the hot
+// row transform no registers
+static __device__ __noinline__ void c2r_partials(float dsum, float osum, double* dst) {
+    const float pv[2] = {dsum, osum};
+    block_partials<2>(pv, dst);
+}
+
 #define H_OF(L) (1 << (L))
 // Row pass 2: transposed half spectrum -> inverse real FFT -> phi rows (accumulated, clamped).
 #ifndef SRSB_C2R_MINB
-#define SRSB_C2R_MINB 1     // resident CTAs per SM asked of ptxas for the <= 256-thread launch-shape instances
+#define SRSB_C2R_MINB (SRSB_C2R_OLD_SMEM ? 3 : 2)   // resident CTAs per SM asked of ptxas for the <= 256-thread
+                                                   // launch-shape instances (2 caps them at 128 registers: without
+                                                   // a cap the monitor reduction let ptxas take 153)
 #endif
 #ifndef SRSB_C2R_MINB_BIG
 #define SRSB_C2R_MINB_BIG 1 // the same for the 512-thread instances (H = 4096: C5)
 #endif
 #ifndef SRSB_C2R_LATE_OLD
 #define SRSB_C2R_LATE_OLD 0 // 1: fetch the accumulation source after the FFT (fewer live registers)
+#endif
+#ifndef SRSB_C2R_OLD_SMEM
+#define SRSB_C2R_OLD_SMEM 0 // 1: the launch-shape instances stage the accumulation source (psi) into shared memory
+                            // with cp.async at their start instead of holding it in 32 registers through the FFT
+                            // (the host then adds rpc * 2H floats of dynamic shared memory to the c2r launch).
+                            // Measured on C3: 0.258 ms per launch (78 registers, 3 CTAs / SM) against 0.189 ms
+                            // with psi in registers (128 registers, 2 CTAs / SM): off
 #endif
 template <int LOGH, int LOGE, int LRPC = -1, int LG = -1>
 __global__ void __launch_bounds__(LRPC >= 0 ? ((H_OF(LOGH) / (1 << LOGE)) << (LRPC >= 0 ? LRPC : 0)) : 512,
@@ -539,9 +557,18 @@ k_rows_c2r(const float2* __restrict__ spec, float* __restrict__ phi,
         if (block_ahead_2d(SRSB_C2R_PF_DIST, bx, by))
             bulk_prefetch_l2(phi + by * a.plane + (long long)(bx * rpc) * (2 * H), (uint32_t)(rpc * 2 * H * 4));
     }
-    // accumulation source (phi of the previous sweep), fetched first: its latency hides behind the FFT
+    // accumulation source (phi of the previous sweep), fetched first: its latency hides behind the FFT.
+    // OSM: into shared memory by cp.async (no registers held across the FFT), else into registers
+    constexpr bool OSM = SRSB_C2R_OLD_SMEM && LRPC >= 0 && !SRSB_C2R_LATE_OLD;
+    float2* old_sm = smem2 + (size_t)rpc * a.SR + (size_t)grp * H;
     float2 old[E];
-    if (!SRSB_C2R_LATE_OLD && a.accum) {
+    if (OSM && a.accum) {
+#pragma unroll
+        for (int u = 0; u < E; u++)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(old_sm + t + u * T)),
+                         "l"(out + t + u * T) : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    } else if (!SRSB_C2R_LATE_OLD && a.accum) {
 #pragma unroll
         for (int u = 0; u < E; u++) old[u] = out[t + u * T];
     }
@@ -604,6 +631,11 @@ k_rows_c2r(const float2* __restrict__ spec, float* __restrict__ phi,
 #pragma unroll
         for (int u = 0; u < E; u++) old[u] = out[t + u * T];
     }
+    if (OSM && a.accum) {   // each thread reads back exactly the values it copied
+        asm volatile("cp.async.wait_all;" ::: "memory");
+#pragma unroll
+        for (int u = 0; u < E; u++) old[u] = old_sm[t + u * T];
+    }
     float dsum = 0.f, osum = 0.f;
 #pragma unroll
     for (int u = 0; u < E; u++) {
@@ -623,23 +655,15 @@ k_rows_c2r(const float2* __restrict__ spec, float* __restrict__ phi,
             osum += old[u].x * old[u].x + old[u].y * old[u].y;
         }
     }
+#ifdef SRSB_C2R_STATS_ATOMIC   // A/B reference only (nondeterministic sums)
     if (a.stats && a.accum) {
-        double* st = a.stats + (long long)b * a.stats_stride;
-        if ((blockDim.x & 31) == 0) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
-                osum += __shfl_xor_sync(0xffffffffu, osum, o);
-            }
-            if ((tid & 31) == 0) {
-                atomicAdd(st, (double)dsum);
-                atomicAdd(st + 1, (double)osum);
-            }
-        } else {
-            atomicAdd(st, (double)dsum);
-            atomicAdd(st + 1, (double)osum);
-        }
+        atomicAdd(a.stats, (double)dsum);
+        atomicAdd(a.stats + 1, (double)osum);
     }
+#else
+    if (a.stats && a.accum)   // this CTA's partial sums -> its slot (image-major), reduced in a fixed order
+        c2r_partials(dsum, osum, a.stats + ((long long)b * gridDim.x + blockIdx.x) * 2);
+#endif
 }
 
 }  // namespace srsb

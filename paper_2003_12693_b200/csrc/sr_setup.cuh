@@ -7,6 +7,7 @@
 // provided its ghost rows hold the neighbouring slabs' rows.
 #pragma once
 #include <cuda_runtime.h>
+#include "sr_reduce.cuh"
 
 namespace srsb {
 
@@ -89,7 +90,7 @@ __global__ void k_init_w(const float* __restrict__ phi, float* __restrict__ w, f
 }
 
 // NEXT-1 outer convergence: per image sum (phi - prev)^2 and sum prev^2 over the local rows, then
-// prev = phi.  grid (blocks, batch); out[img * stride + 0 / 1].
+// prev = phi.  grid (blocks, batch); out = per-CTA partials [img][blockIdx.x][2] (stride unused).
 __global__ void k_phi_change(const float* __restrict__ phi, float* __restrict__ prev, double* __restrict__ out,
                              int M, int N, long long plane, int stride) {
     const int img = blockIdx.y;
@@ -103,15 +104,8 @@ __global__ void k_phi_change(const float* __restrict__ phi, float* __restrict__ 
         o2 += b * b;
         q[i] = a;
     }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        d2 += __shfl_xor_sync(0xffffffffu, d2, o);
-        o2 += __shfl_xor_sync(0xffffffffu, o2, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        atomicAdd(out + (long long)img * stride, (double)d2);
-        atomicAdd(out + (long long)img * stride + 1, (double)o2);
-    }
+    const float pv[2] = {d2, o2};   // per-CTA partials, reduced in a fixed order (k_reduce_partials)
+    block_partials<2>(pv, out + ((long long)img * gridDim.x + blockIdx.x) * 2);
 }
 
 }  // namespace srsb

@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include "sr_f32x2.cuh"
 #include "sr_tma.cuh"
+#include "sr_reduce.cuh"
 
 namespace srsb {
 
@@ -208,15 +209,13 @@ struct StencilArgs {
     int stats_stride;  // doubles per image in stats
 };
 
-// warp-sum of v, one double atomicAdd per warp (monitor only); partial warps add per thread
-__device__ __forceinline__ void warp_accumulate(double* dst, float v) {
-    if (__activemask() == 0xffffffffu) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if ((threadIdx.x & 31) == 0) atomicAdd(dst, (double)v);
-    } else {
-        atomicAdd(dst, (double)v);
-    }
+// NEXT-1 monitor: this CTA's Eq. (22) partial sums -> its slot of the partials buffer a.stats
+// (grid = tiles_x x tiles_y x batch; slot = image-major tile index, 4 doubles), summed per image in a
+// fixed order by k_reduce_partials (sr_reduce.cuh): deterministic, no atomics.
+__device__ __forceinline__ void monitor_partials(const StencilArgs& a, float e_g, float e_a, float e_r, float e_pen) {
+    const float v[4] = {e_g, e_a, e_r, e_pen};
+    const long long slot = ((long long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    block_partials<4>(v, a.stats + slot * 4);
 }
 
 #ifndef SRSB_ST_RT
@@ -563,16 +562,17 @@ __device__ __forceinline__ void wb_tile(float4* __restrict__ U, const float* __r
     __syncthreads();
     const int r0 = threadIdx.y * ST_RT, c0 = threadIdx.x * ST_CT;
     const int gj = col0 + c0;
-    if (gj >= N || row0 + r0 >= M) return;
+    const bool active = gj < N && row0 + r0 < M;
+    if (!MON && !active) return;   // the monitor variant keeps every thread for its CTA reduction
     float2 v[ST_RT][ST_CT];
-    window_block<R, SHAPE>(U, r0, c0, a.e, v);
+    if (active) window_block<R, SHAPE>(U, r0, c0, a.e, v);
     bool bad = false;
     constexpr int CT = ST_CT;
     float e_g = 0.f, e_a = 0.f, e_r = 0.f, e_pen = 0.f;   // monitor partial sums (Eq. 22 terms)
 #pragma unroll
     for (int i = 0; i < ST_RT; i++) {
         const int gi = row0 + r0 + i;
-        if (gi >= M) break;
+        if (!active || gi >= M) break;
         const int gig = gi + a.row_off;   // global row
         const long long o = (long long)gi * N + gj;
         float p_[CT + 1], pn_[CT], b1_[CT], b2_[CT], g_[CT];
@@ -613,13 +613,7 @@ __device__ __forceinline__ void wb_tile(float4* __restrict__ U, const float* __r
         }
     }
     if (UPDATE_B && bad) atomicOr(flag, 1);
-    if (MON) {
-        double* st = a.stats + (long long)img * a.stats_stride;
-        warp_accumulate(st + 0, e_g);
-        warp_accumulate(st + 1, e_a);
-        warp_accumulate(st + 2, e_r);
-        warp_accumulate(st + 3, e_pen);
-    }
+    if (MON) monitor_partials(a, e_g, e_a, e_r, e_pen);
 }
 
 // One CTA per tile (grid = tiles_x x tiles_y x batch).  A persistent variant with one-tile-ahead L2
@@ -1009,8 +1003,8 @@ __global__ void __launch_bounds__(256, SRSB_TMA_MINB) k_wb_tma(const __grid_cons
         tma_load_3d(B2s, &maps.bt, &bar[1], col0, ar, 2 * img + 1);
         tma_load_3d(Gs, &maps.g, &bar[1], col0, ar, img);
     }
-    if (!active) return;
-    mbar_wait(&bar[1], 0);
+    if (!MON && !active) return;   // the monitor variant keeps every thread for its CTA reduction
+    if (active) mbar_wait(&bar[1], 0);
     constexpr int CT = ST_CT;
     bool bad = false;
     float e_g = 0.f, e_a = 0.f, e_r = 0.f, e_pen = 0.f;
@@ -1021,7 +1015,7 @@ __global__ void __launch_bounds__(256, SRSB_TMA_MINB) k_wb_tma(const __grid_cons
 #pragma unroll
     for (int i = 0; i < G::RT; i++) {
         const int tr = r0 + i, gi = row0 + tr;
-        if (gi >= M) break;
+        if (!active || gi >= M) break;
         const int gig = gi + a.row_off;
         const float* prow = Ps + (G::HR + tr) * G::PW + G::CA + c0;
         const float2 P = *reinterpret_cast<const float2*>(prow);
@@ -1052,13 +1046,7 @@ __global__ void __launch_bounds__(256, SRSB_TMA_MINB) k_wb_tma(const __grid_cons
         }
     }
     if (UPDATE_B && bad) atomicOr(flag, 1);
-    if (MON) {
-        double* st = a.stats + (long long)img * a.stats_stride;
-        warp_accumulate(st + 0, e_g);
-        warp_accumulate(st + 1, e_a);
-        warp_accumulate(st + 2, e_r);
-        warp_accumulate(st + 3, e_pen);
-    }
+    if (MON) monitor_partials(a, e_g, e_a, e_r, e_pen);
 }
 
 // MON: the NEXT-1 monitor variant (Eq. 22 energy partial sums), used only when monitoring is on

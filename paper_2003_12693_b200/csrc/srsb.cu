@@ -113,6 +113,8 @@ struct sr_sb_ctx {
     // NEXT-4 AOS phi solver: LR factors of (I - 2 tau mu A) along columns (M) and rows (N)
     float *aos_cpM = nullptr, *aos_rM = nullptr, *aos_cpN = nullptr, *aos_rN = nullptr;
     double* conv = nullptr;        // [batch][2] sums of the outer change
+    double* mon_part = nullptr;    // per-CTA monitor partials (sr_reduce.cuh): [wb tiles][4] | [S][c2r CTAs][2] | [conv][2]
+    size_t part_c2r = 0, part_conv = 0;   // offsets (doubles) of the c2r and outer-change regions
     // sr_sb_profile
     bool prof = false;
     std::vector<cudaEvent_t> ev_pool;
@@ -121,6 +123,8 @@ struct sr_sb_ctx {
 };
 
 namespace {
+
+constexpr int kConvBlocks = 64;   // CTAs per image of k_phi_change (sr_sb_iterate_until)
 
 sr_status fail(sr_sb_ctx* c, sr_status st, const std::string& msg) {
     if (c) c->err = msg;
@@ -283,6 +287,7 @@ sr_status configure(sr_sb_ctx* c) {
         c->rgrid_inv = dim3(Ml / ri, B, 1);
         c->rblock_inv = dim3(ri * T_h, 1, 1);
         c->rsmem_inv = ri * c->ra_inv.SR * (int)sizeof(float2);
+        if (SRSB_C2R_OLD_SMEM) c->rsmem_inv += ri * H * (int)sizeof(float2);   // psi staged in shared memory
         c->rinv = pick_row_inv_shape(lgH, ilog2(ri), ilog2(G));
     }
     c->ca.H = H;
@@ -545,11 +550,15 @@ void enq_c2r(sr_sb_ctx* c, float* out, float clip, int accum, int sweep = -1) {
     FftRowArgs ra = c->ra_inv;
     ra.accum = accum;
     ra.clip = clip;
-    ra.stats = (c->stats && sweep >= 0) ? c->stats + 4 + 2 * sweep : nullptr;
+    const bool mon = c->stats && sweep >= 0;
+    ra.stats = mon ? c->mon_part + c->part_c2r + (size_t)sweep * c->rgrid_inv.x * c->p.batch * 2 : nullptr;
     ra.stats_stride = c->stats_stride;
     prof_begin(c);
     c->rinv<<<c->rgrid_inv, c->rblock_inv, c->rsmem_inv, c->s>>>(c->spec, out, c->twH, c->twR, ra);
     prof_end(c, SR_K_ROWS_C2R);
+    if (mon)   // ||phi^{s+1} - phi^s||^2, ||phi^s||^2 per image, summed in a fixed order
+        k_reduce_partials<<<c->p.batch * 2, 32, 0, c->s>>>(ra.stats, (int)c->rgrid_inv.x, 2, c->stats + 4 + 2 * sweep,
+                                                           c->stats_stride);
 }
 void enq_rhs(sr_sb_ctx* c, float* F) {
     prof_begin(c);
@@ -590,6 +599,11 @@ void enq_wb_pass(sr_sb_ctx* c, int last) {
                                                    c->sa);
     }
     prof_end(c, SR_K_WB);
+    if (mon) {   // Eq. (22) terms per image from the per-tile partials, in a fixed order
+        const dim3 gr = c->rhs_tma ? c->tgrid : c->sgrid;
+        k_reduce_partials<<<c->p.batch * 4, 32, 0, c->s>>>(c->mon_part, (int)(gr.x * gr.y), 4, c->stats,
+                                                           c->stats_stride);
+    }
     c->wcur ^= 1;
 }
 
@@ -1396,15 +1410,23 @@ sr_status sr_sb_set_monitor(sr_sb_ctx* c, int enable) {
         CK(cudaMalloc((void**)&c->prev_phi, sizeof(float) * c->pitch * c->p.batch));
         CK(cudaMemset(c->prev_phi, 0, sizeof(float) * c->pitch * c->p.batch));
         CK(cudaMalloc((void**)&c->conv, sizeof(double) * 2 * c->p.batch));
+        const size_t B = c->p.batch;
+        const size_t nwb = (size_t)c->sgrid.x * std::max(c->sgrid.y, c->tgrid.y) * B * 4;
+        const size_t nc2r = (size_t)c->p.S * c->rgrid_inv.x * B * 2;
+        c->part_c2r = nwb;
+        c->part_conv = nwb + nc2r;
+        CK(cudaMalloc((void**)&c->mon_part, sizeof(double) * (nwb + nc2r + kConvBlocks * B * 2)));
     } else if (!enable && c->stats) {
         CK(cudaFree(c->stats));
         CK(cudaFree(c->prev_phi));
         CK(cudaFree(c->conv));
+        CK(cudaFree(c->mon_part));
         c->stats = nullptr;
         c->prev_phi = nullptr;
         c->conv = nullptr;
+        c->mon_part = nullptr;
     }
-    c->sa.stats = c->stats;
+    c->sa.stats = c->mon_part;
     c->sa.stats_stride = c->stats_stride;
     drop_graphs(c);   // the captured graphs bake the kernel arguments: rebuild on the next iterate
     return SR_OK;
@@ -1425,20 +1447,20 @@ sr_status sr_sb_iterate_until(sr_sb_ctx* c, int K_max, double tol, int every, in
     if (!c->stats) return fail(c, SR_ERR_STATE, "monitor not enabled (sr_sb_set_monitor)");
     DevGuard dg(c->device);
     const int B = c->p.batch;
-    const dim3 grd(64, B), blk(256);
+    const dim3 grd(kConvBlocks, B), blk(256);
     const size_t off = (size_t)c->gh * c->p.N;
     std::vector<double> cv(2 * B);
     // snapshot phi^k
-    CK(cudaMemsetAsync(c->conv, 0, sizeof(double) * 2 * B, c->s));
-    k_phi_change<<<grd, blk, 0, c->s>>>(c->phi, c->prev_phi + off, c->conv, c->Ml, c->p.N, c->pitch, 2);
+    double* part = c->mon_part + c->part_conv;
+    k_phi_change<<<grd, blk, 0, c->s>>>(c->phi, c->prev_phi + off, part, c->Ml, c->p.N, c->pitch, 2);
     int done = 0;
     while (done < K_max) {
         const int n = (K_max - done) < every ? (K_max - done) : every;
         RET(sr_sb_iterate(c, n));
         done += n;
         // outer relative change ||phi^k - phi^{k-n}|| / (||phi^{k-n}|| + 1e-6)  (SPEC's outer rule)
-        CK(cudaMemsetAsync(c->conv, 0, sizeof(double) * 2 * B, c->s));
-        k_phi_change<<<grd, blk, 0, c->s>>>(c->phi, c->prev_phi + off, c->conv, c->Ml, c->p.N, c->pitch, 2);
+        k_phi_change<<<grd, blk, 0, c->s>>>(c->phi, c->prev_phi + off, part, c->Ml, c->p.N, c->pitch, 2);
+        k_reduce_partials<<<B * 2, 32, 0, c->s>>>(part, kConvBlocks, 2, c->conv, 2);
         CK(cudaMemcpyAsync(cv.data(), c->conv, sizeof(double) * 2 * B, cudaMemcpyDeviceToHost, c->s));
         CK(cudaStreamSynchronize(c->s));
         double worst = 0.0;
@@ -1473,7 +1495,7 @@ void sr_sb_destroy(sr_sb_ctx* c) {
     drop_graphs(c);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     void* ptrs[] = {c->phi_base, c->F_base, c->w_base[0], c->w_base[1], c->b_base, c->g_base, c->spec,
-                    c->spec_cols, c->twH, c->twM, c->twR, c->cM, c->cN, c->sym, c->flag, c->stats, c->prev_phi, c->conv,
+                    c->spec_cols, c->twH, c->twM, c->twR, c->cM, c->cN, c->sym, c->flag, c->stats, c->prev_phi, c->conv, c->mon_part,
                     c->aos_cpM, c->aos_rM, c->aos_cpN, c->aos_rN};
     for (void* q : ptrs)
         if (q) cudaFree(q);

@@ -406,6 +406,41 @@ def test_monitor_energy_and_sweep_changes(S, orc):
         assert got["sweep_change"] == pytest.approx(changes, rel=1e-3)
 
 
+def test_monitor_reductions_are_deterministic(S):
+    """The monitor sums (Eq. 22 terms, per-sweep changes, the outer change of iterate_until) come from
+    per-CTA partials summed in a fixed order (sr_reduce.cuh), not atomics: bitwise equal across runs,
+    also through the TMA-free stencil path and on a batch with ragged tiles."""
+    from synth import make_config
+    cfg = make_config("c2")
+    p = cfg["params"]
+
+    def run(env=None):
+        import os
+        old = os.environ.get("SRSB_TMA")
+        if env is not None:
+            os.environ["SRSB_TMA"] = env
+        try:
+            with _solver(S, 512, 512, 1, p) as sv:
+                sv.set_image(_cuda(cfg["image"]), _cuda(cfg["phi0"]))
+                sv.set_monitor(True)
+                sv.iterate(3)
+                raw = [m["raw"] for m in sv.monitor()]
+                k, ch = sv.iterate_until(6, 0.0, every=3)
+                sv.sync()
+        finally:
+            if env is not None:
+                if old is None:
+                    del os.environ["SRSB_TMA"]
+                else:
+                    os.environ["SRSB_TMA"] = old
+        return raw, ch
+    a, b, c = run(), run(), run()
+    assert a == b == c
+    d, e = run("0"), run("0")
+    assert d == e
+    np.testing.assert_allclose(np.asarray(d[0]), np.asarray(a[0]), rtol=1e-5, atol=1e-6)
+
+
 def test_iterate_until_outer_change(S, orc):
     """sr_sb_iterate_until stops at the first check whose relative phi change (over `every`
     iterations) is <= tol; the reported change matches the oracle trajectory's at that point."""

@@ -68,7 +68,7 @@ def load(name: str, image: np.ndarray, phi0: np.ndarray, params: dict, K: int, i
     return rec
 
 
-def compute(name: str, image_index: int | None, ensemble: int, log=print) -> str:
+def compute(name: str, image_index: int | None, ensemble: int, log=print, out_dir: str | None = None) -> str:
     import oracle as orc
     from synth import make_config
 
@@ -96,8 +96,10 @@ def compute(name: str, image_index: int | None, ensemble: int, log=print) -> str
         agree.append(float((mm == mask).mean()))
         counts.append(int(orc.label(mm)[0]))
         log(f"  member {m}: agreement {agree[-1]:.6f} count4 {counts[-1]} ({time.time() - t0:.0f} s)")
-    os.makedirs(OUT, exist_ok=True)
+    os.makedirs(out_dir or OUT, exist_ok=True)
     path = cache_path(name, image_index)
+    if out_dir:
+        path = os.path.join(out_dir, os.path.basename(path))
     np.savez_compressed(path, key=np.array(key), shape=np.array(mask.shape), packed=np.packbits(mask.ravel()),
                         count4=np.array(count), K=np.array(K), ens_agree=np.array(agree, dtype=np.float64),
                         ens_count=np.array(counts, dtype=np.int64), wall_s=np.array(time.time() - t0),
@@ -111,12 +113,14 @@ def main(argv=None):
     ap.add_argument("config", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--images", type=int, nargs="*", default=None, help="C3 image indices")
     ap.add_argument("--ensemble", type=int, default=0)
+    ap.add_argument("--out", default=None, help="write the records here instead of tests/golden/masks "
+                                                 "(e.g. gpurun_out/ when the oracle runs on a GPU box's host cores)")
     a = ap.parse_args(argv)
     if a.config == "c3":
         for i in (a.images if a.images is not None else [0, 1, 2, 3]):
-            compute("c3", i, a.ensemble)
+            compute("c3", i, a.ensemble, out_dir=a.out)
     else:
-        compute(a.config, None, a.ensemble)
+        compute(a.config, None, a.ensemble, out_dir=a.out)
 
 
 if __name__ == "__main__":

@@ -147,7 +147,10 @@ __device__ __forceinline__ void fft_stages(float2 (&v)[1 << LOGE], float2* __res
 #pragma unroll
         for (int q = 0; q < Q; q++)
 #pragma unroll
-            for (int r = 0; r < R; r++) v[q + r * Q] = sm[pad16(t + q * T + r * (N / R))];
+            for (int r = 0; r < R; r++) {
+                SRSB_CHK(&sm[pad16(t + q * T + r * (N / R))], 8);
+                v[q + r * Q] = sm[pad16(t + q * T + r * (N / R))];
+            }
         fft_bar<NBAR>();
     }
 #pragma unroll
@@ -185,7 +188,10 @@ __device__ __forceinline__ void fft_stages(float2 (&v)[1 << LOGE], float2* __res
         } else {
             const int base = (j >> LOGNS) * (NS * R) + k;
 #pragma unroll
-            for (int r = 0; r < R; r++) sm[pad16(base + r * NS)] = x[r];
+            for (int r = 0; r < R; r++) {
+                SRSB_CHK(&sm[pad16(base + r * NS)], 8);
+                sm[pad16(base + r * NS)] = x[r];
+            }
         }
     }
     if constexpr (!LAST) {
@@ -347,6 +353,7 @@ __device__ __forceinline__ void sym_stage(const FftColArgs& a, int M, int k2, in
 #pragma unroll
     for (int u = 0; u < E; u++) {
         const int k1 = t + u * T;
+        SRSB_CHK(st + k1, 4);
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(st + k1)),
                      "l"(a.sym + (size_t)k2 * M + k1) : "memory");
     }
@@ -588,6 +595,7 @@ k_rows_c2r(const float2* __restrict__ spec, float* __restrict__ phi,
         }
 #pragma unroll
         for (int u = 0; u < E / 2; u++) {
+            SRSB_CHK(&smem2[sidx[u] + a.SR], 8);
             smem2[sidx[u]] = make_float2(tmp[u].x, tmp[u].y);
             smem2[sidx[u] + a.SR] = make_float2(tmp[u].z, tmp[u].w);
         }
@@ -605,7 +613,10 @@ k_rows_c2r(const float2* __restrict__ spec, float* __restrict__ phi,
             sidx[u] = rr * a.SR + pad16(k2);
         }
 #pragma unroll
-        for (int u = 0; u < E; u++) smem2[sidx[u]] = tmp[u];
+        for (int u = 0; u < E; u++) {
+            SRSB_CHK(&smem2[sidx[u]], 8);
+            smem2[sidx[u]] = tmp[u];
+        }
     }
     __syncthreads();
     float2* sm = smem2 + grp * a.SR;
@@ -613,6 +624,8 @@ k_rows_c2r(const float2* __restrict__ spec, float* __restrict__ phi,
 #pragma unroll
     for (int u = 0; u < E; u++) {
         const int k = t + u * T;
+        SRSB_CHK(&sm[pad16(k)], 8);
+        SRSB_CHK(&sm[pad16(H - k)], 8);
         const float2 X = sm[pad16(k)];
         if (k == 0) {
             // X.x = X[0], X.y = X[N/2]: Z[0] = E[0] + i O[0], E = (X0 + Xh)/2, O = (X0 - Xh)/2

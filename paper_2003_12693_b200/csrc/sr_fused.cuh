@@ -117,7 +117,10 @@ __global__ void __launch_bounds__(256, SRSB_TMA_MINB) k_rhs_r2c(const __grid_con
     if (active) {
 #pragma unroll
         for (int i = 0; i < G::RT; i++)
-            if (row0 + r0 + i < M) *reinterpret_cast<float2*>(Dt + (r0 + i) * G::TW + c0) = res[i];
+            if (row0 + r0 + i < M) {
+                SRSB_CHK(Dt + (r0 + i) * G::TW + c0, 8);
+                *reinterpret_cast<float2*>(Dt + (r0 + i) * G::TW + c0) = res[i];
+            }
     }
     // the band's tiles of D are complete in the cluster's shared memory
     cluster_arrive();
@@ -132,10 +135,12 @@ __global__ void __launch_bounds__(256, SRSB_TMA_MINB) k_rhs_r2c(const __grid_con
 #pragma unroll
         for (int u = 0; u < E; u++) {
             const int k2 = 2 * (t + u * T);
+            SRSB_CHK(Dt + br * G::TW + (k2 % G::TW), 8);
             x[u] = ld_dsmem_f2(Dt + br * G::TW + (k2 % G::TW), (uint32_t)(k2 / G::TW));
         }
         cluster_arrive();                        // this thread's remote reads are done
         float2* srow = Fr + grp * SR;
+        SRSB_CHK(srow, SR * 8);
         fft_stages<LOGH, LOGE, 0, false, NFT>(x, srow, t, twH);
 #pragma unroll
         for (int u = 0; u < E; u++) srow[pad16(t + u * T)] = x[u];

@@ -346,6 +346,8 @@ __device__ __forceinline__ void window_block(const float4* __restrict__ U, int r
     for (int rr = 0; rr < RT + 2 * R; rr++) {
         float2 a[2 * NC];
         const float4* row = U + (r0 + rr) * LDC;
+        SRSB_CHK(row + swz(chunk0), 16);
+        SRSB_CHK(row + swz(chunk0 + NC - 1), 16);
 #pragma unroll
         for (int k = 0; k < NC; k++) {
             const float4 q4 = row[swz(chunk0 + k)];
@@ -738,6 +740,9 @@ __device__ __forceinline__ void stage_u_tma(float4* __restrict__ U, const float*
         const float2 h = reg_h2<LEQ>(P, a.reg);
         const float2 hx = mul2(h, X), hy = mul2(h, Y);
         const bool in = gr >= 0 && gr < a.Mg;
+        SRSB_CHK(Ps + o, 8);
+        SRSB_CHK(W2s + o, 8);
+        SRSB_CHK(&U[r * G::LDC + swz(f)], 16);
         U[r * G::LDC + swz(f)] = in ? make_float4(hx.x, hy.x, hx.y, hy.y) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 }
@@ -769,6 +774,12 @@ __device__ __forceinline__ void rhs_points_tma(const float* Ps, const float* W1s
         const float* w1r = W1s + (G::HR + tr) * G::PW + G::CA + c0;
         const float* w2r = W2s + (G::HR + tr) * G::PW + G::CA + c0;
         const float* b1r = B1s + (1 + tr) * G::BW + 4 + c0;
+        SRSB_CHK(prow - 1, 4 * (ST_CT + 2));
+        SRSB_CHK(prow + G::PW, 8);
+        SRSB_CHK(W2s + (G::HR + tr) * G::PW + G::CA + c0 - 1, 12);
+        SRSB_CHK(b1r - G::BW, 8);
+        SRSB_CHK(B2s + (1 + tr) * G::BW + 4 + c0 - 1, 12);
+        SRSB_CHK(Gs + tr * G::TW + c0, 8);
         const float* b2r = B2s + (1 + tr) * G::BW + 4 + c0;
         const float2 Pn = *reinterpret_cast<const float2*>(prow + G::PW);
         float2 Pu = Pc, Pd = Pn;
@@ -1021,6 +1032,10 @@ __global__ void __launch_bounds__(256, SRSB_TMA_MINB) k_wb_tma(const __grid_cons
         const float2 P = *reinterpret_cast<const float2*>(prow);
         const float2 Pn = *reinterpret_cast<const float2*>(prow + G::PW);
         const float p_[CT + 1] = {P.x, P.y, prow[CT]}, pn_[CT] = {Pn.x, Pn.y};
+        SRSB_CHK(prow, 4 * (CT + 1));
+        SRSB_CHK(prow + G::PW, 8);
+        SRSB_CHK(B1s + tr * G::TW + c0, 8);
+        SRSB_CHK(Gs + tr * G::TW + c0, 8);
         const float2 B1 = *reinterpret_cast<const float2*>(B1s + tr * G::TW + c0);
         const float2 B2 = *reinterpret_cast<const float2*>(B2s + tr * G::TW + c0);
         const float2 Gv = *reinterpret_cast<const float2*>(Gs + tr * G::TW + c0);

@@ -5,10 +5,33 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdio>
 
 namespace srsb {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+// Checked build (-DSRSB_CHECKS, tools/checked_lib.py): every staged shared-memory access named with
+// SRSB_CHK(ptr, bytes) must lie inside the launch's dynamic shared memory, else the kernel prints the
+// site and traps.  Stands in for compute-sanitizer's memcheck on the shared-memory side, which this
+// pool does not allow.  Compiles to nothing in the normal build.
+#ifdef SRSB_CHECKS
+static __device__ __noinline__ void srsb_chk_fail(const char* file, int line, uint32_t off, uint32_t n, uint32_t size) {
+    printf("SRSB_CHECKS: %s:%d shared access [%u, %u) outside dynamic shared memory of %u bytes (block %d,%d,%d thread %d,%d)\n",
+           file, line, off, off + n, size, blockIdx.x, blockIdx.y, blockIdx.z, threadIdx.x, threadIdx.y);
+    __trap();
+}
+__device__ __forceinline__ void srsb_chk(const void* p, uint32_t n, const char* file, int line) {
+    extern __shared__ unsigned char srsb_chk_base[];
+    uint32_t size;
+    asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(size));
+    const uint32_t off = smem_u32(p) - smem_u32(srsb_chk_base);
+    if (off > size || n > size - off) srsb_chk_fail(file, line, off, n, size);
+}
+#define SRSB_CHK(p, n) ::srsb::srsb_chk((p), (n), __FILE__, __LINE__)
+#else
+#define SRSB_CHK(p, n) ((void)0)
+#endif
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");

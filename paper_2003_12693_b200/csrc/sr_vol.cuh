@@ -29,6 +29,7 @@ struct VolArgs {
     int w_proj;
     float b_max;
     int aos;           // unused in 3-D (FFT solver only); kept 0
+    int band_skip;     // 1: ball sums only in the narrow band (exact; SRSB_BAND_SKIP=0 turns it off)
 };
 
 // ------------------------------------------------------------------ 2-D FFT of one spectrum plane
@@ -164,6 +165,34 @@ __device__ __forceinline__ void vol_window(const float* __restrict__ U, const fl
     }
 }
 
+// Narrow band in 3-D (as needs_v in sr_stencil.cuh): the thread's V_TZ voxels (z0 + 0..3, y, x) that
+// lie in the volume need v only where h / h' != 0; a tile none of whose voxels does skips the staging.
+template <bool LEQ>
+__device__ __forceinline__ bool vol_needs_v(const float* __restrict__ phi, const VolArgs& a, int z0, int y, int x) {
+    if (x >= a.N || y >= a.M) return false;
+    bool need = false;
+#pragma unroll
+    for (int zz = 0; zz < V_TZ; zz++) {
+        const int z = z0 + zz;
+        if (z >= a.D) break;
+        need |= needs_v<LEQ>(__ldg(phi + ((long long)z * a.M + y) * a.N + x), a.reg);
+    }
+    return need;
+}
+template <int R, int SHAPE, bool LEQ>
+__device__ __forceinline__ void vol_v(float* U, const float* __restrict__ phi, const float* __restrict__ w,
+                                      const VolArgs& a, int z0, int y0, int x0, float (&v)[V_TZ][3]) {
+#pragma unroll
+    for (int zz = 0; zz < V_TZ; zz++) v[zz][0] = v[zz][1] = v[zz][2] = 0.f;
+    const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
+    const bool own = !a.band_skip || vol_needs_v<LEQ>(phi, a, z0, y, x);
+    if (__syncthreads_or(own)) {
+        vol_stage_u<R, LEQ>(U, phi, w, a, z0, y0, x0);
+        __syncthreads();
+        if (own && x < a.N && y < a.M) vol_window<R, SHAPE>(U, a.e, v);
+    }
+}
+
 // Eq. (37) in 3-D, increment form: D = tau [ -gamma g |w| delta' + alpha g delta
 //   + 2 beta h' w.v + mu div(b - w) + mu Delta_per psi ].
 template <int R, int SHAPE, bool LEQ>
@@ -173,12 +202,10 @@ __global__ void __launch_bounds__(256) k3_rhs(const float* __restrict__ phi, con
     extern __shared__ float4 smem_v4[];
     float* U = reinterpret_cast<float*>(smem_v4);
     const int x0 = blockIdx.x * V_TX, y0 = blockIdx.y * V_TY, z0 = blockIdx.z * V_TZ;
-    vol_stage_u<R, LEQ>(U, phi, w, a, z0, y0, x0);
-    __syncthreads();
+    float v[V_TZ][3];
+    vol_v<R, SHAPE, LEQ>(U, phi, w, a, z0, y0, x0, v);
     const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
     if (x >= a.N || y >= a.M) return;
-    float v[V_TZ][3];
-    vol_window<R, SHAPE>(U, a.e, v);
     const int D = a.D, M = a.M, N = a.N;
     const long long V = a.vol;
 #pragma unroll
@@ -229,12 +256,10 @@ __global__ void __launch_bounds__(256) k3_wb(const float* __restrict__ phi, cons
     extern __shared__ float4 smem_v4[];
     float* U = reinterpret_cast<float*>(smem_v4);
     const int x0 = blockIdx.x * V_TX, y0 = blockIdx.y * V_TY, z0 = blockIdx.z * V_TZ;
-    vol_stage_u<R, LEQ>(U, phi, w_in, a, z0, y0, x0);
-    __syncthreads();
+    float v[V_TZ][3];
+    vol_v<R, SHAPE, LEQ>(U, phi, w_in, a, z0, y0, x0, v);
     const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
     if (x >= a.N || y >= a.M) return;
-    float v[V_TZ][3];
-    vol_window<R, SHAPE>(U, a.e, v);
     const int D = a.D, M = a.M, N = a.N;
     const long long V = a.vol;
     bool bad = false;

@@ -188,6 +188,10 @@ sr_status configure3(sr_sb3_ctx* c) {
     a.w_proj = p.w_proj;
     a.b_max = p.b_max;
     a.aos = 0;
+    {
+        const char* e = getenv("SRSB_BAND_SKIP");
+        a.band_skip = (e && e[0] == '0') ? 0 : 1;
+    }
     // tables (fp64 -> fp32)
     const double pi = 3.14159265358979323846;
     std::vector<float2> twH(H), twR(H), twM(M), twD(D);

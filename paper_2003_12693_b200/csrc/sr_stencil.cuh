@@ -359,7 +359,7 @@ __device__ __forceinline__ void window_block(const float4* __restrict__ U, int r
 #pragma unroll
         for (int c = 0; c < ST_CT; c++) {
             const int m = OFF + c + R;
-            float2 acc = mul2(ew[0], a[m]);
+            float2 acc = a[m];   // e_0 = exp(0) = 1 exactly: 1 * u is u (no multiply)
             S[0][c] = acc;
 #pragma unroll
             for (int q = 1; q <= R; q++) {
@@ -374,7 +374,8 @@ __device__ __forceinline__ void window_block(const float4* __restrict__ U, int r
                 const int ap = p < 0 ? -p : p;
                 const int L = half_width<R, SHAPE>(ap);
 #pragma unroll
-                for (int c = 0; c < ST_CT; c++) v[i][c] = fma2(ew[ap], S[L][c], v[i][c]);
+                for (int c = 0; c < ST_CT; c++)   // fma(1, S, v) = S + v with one rounding: the same as add
+                    v[i][c] = ap == 0 ? add2(S[L][c], v[i][c]) : fma2(ew[ap], S[L][c], v[i][c]);
             }
         }
     }

@@ -6,3 +6,7 @@ timeout 600 python -m pytest tests/test_gpu_3d.py -q -x > gpurun_out/r2k_3d.log 
 timeout 300 python bench.py --config v3d --steps 3 --warmup 3 --no-cpu --no-e2e > gpurun_out/r2k_v3d.log 2>&1
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:"k_rhs_tma|k_wb_tma|k_rows|k_cols" -s 40 -c 5 -o gpurun_out/r2k_c4 -f python bench.py --config c4 --steps 1 --warmup 0 --iters 12 --no-e2e --no-cpu --no-fft-ref > /dev/null 2>&1; echo ncu4=$?
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:"k_rows|k_cols" -s 6 -c 3 -o gpurun_out/r2k_c5 -f python bench.py --config c5 --steps 1 --warmup 0 --iters 4 --no-e2e --no-cpu --no-fft-ref > /dev/null 2>&1; echo ncu5=$?
+B="python bench.py --no-cpu --no-e2e --no-fft-ref --steps 2 --warmup 3"
+SRSB_CPC=2 timeout 300 $B --config c4 --iters 100 > gpurun_out/r2k_c4_cpc2.log 2>&1
+SRSB_BAND_SKIP=0 timeout 300 $B --config c4 --iters 100 > gpurun_out/r2k_c4_noskip.log 2>&1
+timeout 300 $B --config c4 --iters 100 > gpurun_out/r2k_c4.log 2>&1

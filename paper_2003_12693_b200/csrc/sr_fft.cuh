@@ -215,7 +215,8 @@ struct FftRowArgs {
 
 // Row pass 1: F rows (N = 2H reals) -> transposed packed half spectrum.
 template <int LOGH, int LOGE, int LRPC = -1, int LG = -1>
-__global__ void __launch_bounds__(512) k_rows_r2c(const float* __restrict__ F, float2* __restrict__ spec,
+__global__ void __launch_bounds__((LRPC >= 0 && (((1 << LOGH) >> LOGE) << (LRPC >= 0 ? LRPC : 0)) > 512) ? 1024 : 512)
+k_rows_r2c(const float* __restrict__ F, float2* __restrict__ spec,
                                                    const float2* __restrict__ twH,
                                                    const float2* __restrict__ twR, FftRowArgs a) {
     constexpr int H = 1 << LOGH, E = 1 << LOGE, T = H / E;

@@ -290,6 +290,20 @@ sr_status configure(sr_sb_ctx* c) {
         if (SRSB_C2R_OLD_SMEM) c->rsmem_inv += ri * H * (int)sizeof(float2);   // psi staged in shared memory
         c->rinv = pick_row_inv_shape(lgH, ilog2(ri), ilog2(G));
     }
+    {   // wide r2c (after the c2r took its own shape): with contiguous columns a 1024-thread CTA of 2 x rpc rows
+        // writes 32-byte transposed chunks instead of 16 (C5, H = 4096: rpc = 2 -> 4; SRSB_R2C_WIDE=0: off)
+        const char* ev = std::getenv("SRSB_R2C_WIDE");
+        const int r2 = 2 * rpc;
+        if (G == 1 && !c->slab && rpc * T_h == 512 && r2 <= Ml && !(ev && ev[0] == '0') &&
+            pick_row_fwd_shape(lgH, ilog2(r2), 0) != pick_row_fwd(lgH)) {
+            c->rfwd = pick_row_fwd_shape(lgH, ilog2(r2), 0);
+            c->ra.lg_rpc = ilog2(r2);
+            c->ra.SR = padded(H, r2 >= 16 ? 1 : (16 / r2) & 15);
+            c->rgrid = dim3(Ml / r2, B, 1);
+            c->rblock = dim3(r2 * T_h, 1, 1);
+            c->rsmem = r2 * c->ra.SR * (int)sizeof(float2);
+        }
+    }
     c->ca.H = H;
     c->ca.lg_G = ilog2(G);
     c->ca.lg_cpc = ilog2(cpc);

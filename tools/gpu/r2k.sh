@@ -10,3 +10,7 @@ B="python bench.py --no-cpu --no-e2e --no-fft-ref --steps 2 --warmup 3"
 SRSB_CPC=2 timeout 300 $B --config c4 --iters 100 > gpurun_out/r2k_c4_cpc2.log 2>&1
 SRSB_BAND_SKIP=0 timeout 300 $B --config c4 --iters 100 > gpurun_out/r2k_c4_noskip.log 2>&1
 timeout 300 $B --config c4 --iters 100 > gpurun_out/r2k_c4.log 2>&1
+timeout 300 $B --config c5 --iters 50 > gpurun_out/r2k_c5_wide.log 2>&1
+SRSB_R2C_WIDE=0 timeout 300 $B --config c5 --iters 50 > gpurun_out/r2k_c5_nowide.log 2>&1
+timeout 300 $B --iters 200 > gpurun_out/r2k_c3.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "launch_shape or band_skip or trajectory_c5_small or trajectory_c1" > gpurun_out/r2k_tests2.log 2>&1; echo tests2_rc=$?; tail -2 gpurun_out/r2k_tests2.log

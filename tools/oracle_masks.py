@@ -2,7 +2,7 @@
 
     python tools/oracle_masks.py c2 --ensemble 8
     python tools/oracle_masks.py c3 --images 0 1 2 3
-    python tools/oracle_masks.py c5
+    python tools/oracle_masks.py c5 --K 30      (a truncated horizon: see DESIGN.md §6)
 
 Calls ONLY `oracle/` (the float64 C oracle) and `synth/` (seeded inputs); nothing here touches
 the CUDA path, so every stored value comes from the oracle (task rule: a stored value is written
@@ -48,13 +48,16 @@ def run_key(image: np.ndarray, phi0: np.ndarray, params: dict, K: int) -> str:
     return h.hexdigest()
 
 
-def cache_path(name: str, image_index: int | None = None) -> str:
-    return os.path.join(OUT, f"{name}.npz" if image_index is None else f"{name}_i{image_index}.npz")
+def cache_path(name: str, image_index: int | None = None, K: int | None = None) -> str:
+    """K: a truncated horizon (records of the full-K run carry no suffix)."""
+    stem = name if image_index is None else f"{name}_i{image_index}"
+    return os.path.join(OUT, stem + (f"_k{K}" if K is not None else "") + ".npz")
 
 
-def load(name: str, image: np.ndarray, phi0: np.ndarray, params: dict, K: int, image_index=None) -> dict | None:
+def load(name: str, image: np.ndarray, phi0: np.ndarray, params: dict, K: int, image_index=None,
+         truncated: bool = False) -> dict | None:
     """The cached record for this exact input, or None when it is missing or stale."""
-    p = cache_path(name, image_index)
+    p = cache_path(name, image_index, K if truncated else None)
     if not os.path.exists(p):
         return None
     z = np.load(p)
@@ -68,12 +71,13 @@ def load(name: str, image: np.ndarray, phi0: np.ndarray, params: dict, K: int, i
     return rec
 
 
-def compute(name: str, image_index: int | None, ensemble: int, log=print, out_dir: str | None = None) -> str:
+def compute(name: str, image_index: int | None, ensemble: int, log=print, out_dir: str | None = None,
+            K_override: int | None = None) -> str:
     import oracle as orc
     from synth import make_config
 
     cfg = make_config(name, images=None if image_index is None else [image_index])
-    p, K = cfg["params"], cfg["K"]
+    p, K = cfg["params"], cfg["K"] if K_override is None else K_override
     img, phi0 = cfg["image"][0], cfg["phi0"][0]
     key = run_key(img, phi0, p, K)
     t0 = time.time()
@@ -97,7 +101,7 @@ def compute(name: str, image_index: int | None, ensemble: int, log=print, out_di
         counts.append(int(orc.label(mm)[0]))
         log(f"  member {m}: agreement {agree[-1]:.6f} count4 {counts[-1]} ({time.time() - t0:.0f} s)")
     os.makedirs(out_dir or OUT, exist_ok=True)
-    path = cache_path(name, image_index)
+    path = cache_path(name, image_index, K_override)
     if out_dir:
         path = os.path.join(out_dir, os.path.basename(path))
     np.savez_compressed(path, key=np.array(key), shape=np.array(mask.shape), packed=np.packbits(mask.ravel()),
@@ -115,12 +119,13 @@ def main(argv=None):
     ap.add_argument("--ensemble", type=int, default=0)
     ap.add_argument("--out", default=None, help="write the records here instead of tests/golden/masks "
                                                  "(e.g. gpurun_out/ when the oracle runs on a GPU box's host cores)")
+    ap.add_argument("--K", type=int, default=None, help="truncated horizon (record named <cfg>_k<K>.npz)")
     a = ap.parse_args(argv)
     if a.config == "c3":
         for i in (a.images if a.images is not None else [0, 1, 2, 3]):
-            compute("c3", i, a.ensemble, out_dir=a.out)
+            compute("c3", i, a.ensemble, out_dir=a.out, K_override=a.K)
     else:
-        compute(a.config, None, a.ensemble, out_dir=a.out)
+        compute(a.config, None, a.ensemble, out_dir=a.out, K_override=a.K)
 
 
 if __name__ == "__main__":

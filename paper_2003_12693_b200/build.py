@@ -40,12 +40,30 @@ def _deps():
                   glob.glob(os.path.join(INCLUDE, "*.h")))
 
 
+_INC = None
+
+
+def _src_deps(path: str, seen=None) -> set:
+    """Headers a source reaches through #include "..." (resolved in csrc/ and include/), recursively."""
+    import re
+    seen = set() if seen is None else seen
+    for m in re.finditer(r'^\s*#\s*include\s+"([^"]+)"', open(path).read(), re.M):
+        for base in (os.path.dirname(path), CSRC, INCLUDE):
+            q = os.path.normpath(os.path.join(base, m.group(1)))
+            if os.path.exists(q):
+                if q not in seen:
+                    seen.add(q)
+                    _src_deps(q, seen)
+                break
+    return seen
+
+
 def _compile(src: str, force: bool) -> tuple[str, str]:
     obj = os.path.join(OBJ, os.path.basename(src).replace(".cu", ".o"))
     log = obj + ".ptxas.log"
     stamp = obj + ".flags"
     flags = " ".join(ARCH + FLAGS)
-    newest = max(os.path.getmtime(p) for p in [src] + _deps())
+    newest = max(os.path.getmtime(p) for p in [src] + sorted(_src_deps(src)))
     same_flags = os.path.exists(stamp) and open(stamp).read() == flags
     if not force and same_flags and os.path.exists(obj) and os.path.getmtime(obj) >= newest:
         return obj, "cached"

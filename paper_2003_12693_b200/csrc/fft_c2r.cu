@@ -15,6 +15,8 @@ RowInvKernel pick_row_inv(int lg) {
 RowInvKernel pick_row_inv_shape(int lg, int lg_rpc, int lg_G) {
 #define SRSB_SHAPE(LH, LR, LG_) if (lg == LH && lg_rpc == LR && lg_G == LG_) return k_rows_c2r<LH, 4, LR, LG_>;
     SRSB_SHAPE(6, 4, 0) SRSB_SHAPE(8, 3, 0) SRSB_SHAPE(9, 1, 0) SRSB_SHAPE(9, 2, 0) SRSB_SHAPE(9, 3, 0) SRSB_SHAPE(9, 4, 0) SRSB_SHAPE(11, 2, 0) SRSB_SHAPE(11, 2, 1) SRSB_SHAPE(12, 1, 0)
+    // row-major spectrum (G = H; k_cols_tri_rm): one row per CTA
+    SRSB_SHAPE(9, 0, 9) SRSB_SHAPE(9, 1, 9) SRSB_SHAPE(10, 0, 10) SRSB_SHAPE(11, 0, 11) SRSB_SHAPE(12, 0, 12)
 #undef SRSB_SHAPE
     return pick_row_inv(lg);
 }

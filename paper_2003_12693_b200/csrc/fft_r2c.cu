@@ -16,6 +16,8 @@ RowKernel pick_row_fwd_shape(int lg, int lg_rpc, int lg_G) {
 #define SRSB_SHAPE(LH, LR, LG_) if (lg == LH && lg_rpc == LR && lg_G == LG_) return k_rows_r2c<LH, 4, LR, LG_>;
     SRSB_SHAPE(6, 4, 0) SRSB_SHAPE(8, 3, 0) SRSB_SHAPE(9, 3, 0) SRSB_SHAPE(11, 2, 0) SRSB_SHAPE(11, 2, 1) SRSB_SHAPE(12, 1, 0)
     SRSB_SHAPE(12, 2, 0)   // C5 wide: 4 rows x 256 threads, 32-byte transposed chunks (configure(): SRSB_R2C_WIDE)
+    // row-major spectrum (G = H; k_cols_tri_rm): C3 (2 rows per CTA), C4, C5 (1 row), 512-wide rows
+    SRSB_SHAPE(9, 1, 9) SRSB_SHAPE(9, 2, 9) SRSB_SHAPE(10, 0, 10) SRSB_SHAPE(10, 1, 10) SRSB_SHAPE(11, 0, 11) SRSB_SHAPE(12, 0, 12)
 #undef SRSB_SHAPE
     return pick_row_fwd(lg);
 }

@@ -256,19 +256,41 @@ k_rows_r2c(const float* __restrict__ F, float2* __restrict__ spec,
         const float2 wo = cmul(__ldg(&twR[k2]), O);
         return make_float2(Ev.x + wo.x, Ev.y + wo.y);
     };
-    if constexpr (LG == 0 && LRPC >= 1 && E >= 4 && SRSB_R2C_MIRROR) {
+    auto split2 = [&](float2 Za, float2 Zb, float2 tw) -> float2 {   // Zb = Z[H - k]
+        const float2 Zc = conjf2(Zb);
+        const float2 Ev = make_float2(0.5f * (Za.x + Zc.x), 0.5f * (Za.y + Zc.y));
+        const float2 D = make_float2(0.5f * (Za.x - Zc.x), 0.5f * (Za.y - Zc.y));
+        const float2 O = make_float2(D.y, -D.x);  // -i D
+        const float2 wo = cmul(tw, O);
+        return make_float2(Ev.x + wo.x, Ev.y + wo.y);
+    };
+    if constexpr (LG == LOGH && LRPC >= 0 && E >= 2 && LOGH >= 1) {
+        // row-major spectrum (G = H): row m0 + rr is H contiguous complex.  Bins k2 and H - k2 from the same two
+        // shared reads (the split of one is the split of the other with the operands swapped); consecutive
+        // lanes store consecutive (k2) and reverse-consecutive (H - k2) bins: whole lines.  k2 = 0 emits the
+        // packed (X[0], X[N/2]) slot and the self-mirrored bin H / 2.
+        constexpr int LHH = LOGH - 1;
+#pragma unroll
+        for (int u = 0; u < E / 2; u++) {
+            const int e = tid + u * nthr;
+            const int k2 = e & ((1 << LHH) - 1), rr = e >> LHH;   // k2 in [0, H/2)
+            const float2* r0 = smem2 + rr * a.SR;
+            float2* o = out + (size_t)(m0 + rr) * H;
+            if (k2 == 0) {
+                const float2 A0 = r0[0], B0 = r0[pad16(H / 2)];
+                o[0] = make_float2(A0.x + A0.y, A0.x - A0.y);
+                o[H / 2] = split2(B0, B0, __ldg(&twR[H / 2]));
+            } else {
+                const float2 A0 = r0[pad16(k2)], B0 = r0[pad16(H - k2)];
+                o[k2] = split2(A0, B0, __ldg(&twR[k2]));
+                o[H - k2] = split2(B0, A0, __ldg(&twR[H - k2]));
+            }
+        }
+    } else if constexpr (LG == 0 && LRPC >= 1 && E >= 4 && SRSB_R2C_MIRROR) {
         // contiguous columns, bins k2 and H - k2 from the same two shared reads per row (the split of
         // one is the split of the other with the operands swapped); rows 2 rp, 2 rp + 1 of a bin are
         // adjacent -> 16-byte stores.  k2 = 0 also emits the self-mirrored bin H / 2.
         constexpr int LRP = LRPC - 1;
-        auto split2 = [&](float2 Za, float2 Zb, float2 tw) -> float2 {   // Zb = Z[H - k]
-            const float2 Zc = conjf2(Zb);
-            const float2 Ev = make_float2(0.5f * (Za.x + Zc.x), 0.5f * (Za.y + Zc.y));
-            const float2 D = make_float2(0.5f * (Za.x - Zc.x), 0.5f * (Za.y - Zc.y));
-            const float2 O = make_float2(D.y, -D.x);  // -i D
-            const float2 wo = cmul(tw, O);
-            return make_float2(Ev.x + wo.x, Ev.y + wo.y);
-        };
 #pragma unroll
         for (int u = 0; u < E / 4; u++) {
             const int e = tid + u * nthr;
@@ -582,7 +604,25 @@ k_rows_c2r(const float2* __restrict__ spec, float* __restrict__ phi,
     }
     // transposed gather: blockDim = rpc * T threads, rpc * H elements -> exactly E per thread;
     // all E loads are issued before the shared stores
-    if constexpr (LG == 0 && LRPC >= 1) {
+    if constexpr (LG == LOGH && LRPC >= 0 && E >= 2 && LOGH >= 1) {
+        // row-major spectrum (G = H): row m0 + rr is H contiguous complex -> 16-byte loads of two adjacent bins
+        constexpr int LHH = LOGH - 1;
+        float4 tmp[E / 2];
+        int sidx[E / 2];
+#pragma unroll
+        for (int u = 0; u < E / 2; u++) {
+            const int e = tid + u * nthr;
+            const int k2 = 2 * (e & ((1 << LHH) - 1)), rr = e >> LHH;
+            tmp[u] = __ldcs(reinterpret_cast<const float4*>(in + (size_t)(m0 + rr) * H + k2));
+            sidx[u] = rr * a.SR + pad16(k2);
+        }
+#pragma unroll
+        for (int u = 0; u < E / 2; u++) {
+            SRSB_CHK(&smem2[sidx[u] + 1], 8);
+            smem2[sidx[u]] = make_float2(tmp[u].x, tmp[u].y);
+            smem2[sidx[u] + 1] = make_float2(tmp[u].z, tmp[u].w);
+        }
+    } else if constexpr (LG == 0 && LRPC >= 1) {
         // contiguous columns: rows 2 rp, 2 rp + 1 of bin k2 are adjacent -> one 16-byte load per pair
         constexpr int LRP = LRPC - 1;
         float4 tmp[E / 2];

@@ -21,6 +21,7 @@
 
 #include "../../include/srsb.h"
 #include "sr_kernels.h"
+#include "sr_tri.cuh"
 #include <cudaTypedefs.h>
 #include "sr_setup.cuh"
 #include "sr_aos.cuh"
@@ -86,6 +87,14 @@ struct sr_sb_ctx {
     ColKernel cols = nullptr;
     ColPKernel cols_p = nullptr;   // persistent prefetching column solve for long contiguous columns
     int cp_grid = 0, cp_smem = 0, cp_threads = 0;
+    ColTriKernel cols_tri = nullptr;   // cyclic tridiagonal column solve (sr_tri.cuh): whole image, G = 1, M >= 16
+    TriCol* tri_tab = nullptr;         // [H] per-column constants
+    ColTriRmKernel cols_tri_rm = nullptr;   // the same on a row-major spectrum (G = N/2), spec -> spec2
+    float2* spec2 = nullptr;           // row-major mode: the solved spectrum (k_cols_tri_rm is out of place)
+    dim3 trm_grid;
+    int trm_threads = 0, trm_smem = 0, trm_mmax = 0;
+    dim3 tri_grid;
+    int tri_threads = 0, tri_smem = 0, tri_lg_cpc = 0;
     RhsKernel rhs = nullptr;
     RhsTmaKernel rhs_tma = nullptr;   // TMA-staged stencils (default; SRSB_TMA=0 selects k_rhs / k_wb)
     WbTmaKernel wb_tma[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
@@ -206,6 +215,28 @@ bool encode_map3d(CUtensorMap* m, float* base, int N, int rows, int planes, int 
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// carry terms of the chunked recurrences of sr_tri.cuh: the smallest m with rho^m < 2^-48 (rho = r^L), at most
+// one wrap of C chunks (then the series is closed by 1 / (1 - rho^C))
+int tri_carry_terms(double rho, int C, double* clos) {
+    int m = 1;
+    if (rho > 0.0) {
+        const double v = std::ceil(-48.0 * std::log(2.0) / std::log(rho));
+        m = v > (double)C ? C : (int)v;
+    }
+    if (m < 1) m = 1;
+    if (clos) *clos = 1.0;
+    if (m >= C) {
+        m = C;
+        if (clos) *clos = 1.0 / (1.0 - std::pow(rho, C));
+    }
+    return m;
+}
+double tri_ratio(double a, double cc, double* sq_out) {   // r = 2a / (c + sqrt(c^2 - 4 a^2)) of c x_i - a (x_{i-1} + x_{i+1})
+    const double sq = std::sqrt(cc * cc - 4.0 * a * a);
+    if (sq_out) *sq_out = sq;
+    return 2.0 * a / (cc + sq);
+}
+
 sr_status configure(sr_sb_ctx* c) {
     const sr_sb_params& p = c->p;
     const int M = p.M, Ml = c->Ml, N = p.N, H = N / 2, B = p.batch, P = c->nranks;
@@ -243,6 +274,32 @@ sr_status configure(sr_sb_ctx* c) {
         const int v = std::atoi(ev);
         if (v >= 1 && v <= H / P && (v & (v - 1)) == 0) G = v;
     }
+    // Row-major spectrum (G = N/2) with the cyclic tridiagonal column pass on it (sr_tri.cuh, k_cols_tri_rm): both
+    // row passes then move whole lines instead of transposed chunks (measured with the generic row kernels: c2r
+    // C3 0.185 -> 0.153 ms, C4 0.066 -> 0.046, C5 0.312 -> 0.208; r2c C5 0.194 -> 0.166).  Needs few carry terms
+    // (tau mu not extreme), else the transposed layout stays.  Default for N >= 1024 (C1 / C2 measured slower: 313 vs
+    // 342 and 4.2k vs 5.1k Mpx-iter/s); SRSB_SPEC_RM=1 forces it for N >= 64, SRSB_SPEC_RM=0: off.
+    bool rm = false;
+    int rm_mmax = 0;
+    {
+        const char* ev = std::getenv("SRSB_SPEC_RM");
+        const char* et = std::getenv("SRSB_COLS_TRI");
+        const int L = 1 << kTriLogL;
+        if (!c->slab && p.phi_solver == SR_PHI_FFT && H >= (std::getenv("SRSB_SPEC_RM") ? 32 : 512) && M >= L && !(ev && ev[0] == '0') && !(et && et[0] == '0') &&
+            !std::getenv("SRSB_G")) {
+            const double a = (double)p.tau * (double)p.mu;
+            const double r0 = tri_ratio(a, 1.0 + 2.0 * a, nullptr);   // k2 = 0: the slowest decay
+            rm_mmax = tri_carry_terms(std::pow(r0, L), M / L, nullptr);
+            rm = rm_mmax <= kTriRmMaxCarry;
+        }
+    }
+    if (rm) {
+        G = H;
+        if (!std::getenv("SRSB_RPC")) {
+            rpc = 64 / T_h > 1 ? 64 / T_h : 1;   // >= 64 threads per CTA (measured: C3 2-4 rows, C4 / C5 1 row)
+            if (rpc > Ml) rpc = Ml;
+        }
+    }
     c->cols = pick_col(lgM, !c->slab && G == 1, c->use_sym);   // whole image, contiguous columns: immediate-offset access
     c->rfwd = pick_row_fwd_shape(lgH, ilog2(rpc), ilog2(G));
     //  columns per CTA: >= 64 threads, <= 512 (a CTA may cover part of a column group)
@@ -277,7 +334,11 @@ sr_status configure(sr_sb_ctx* c) {
         // per CTA, so the inverse pass may take its own (SRSB_RPC_INV, tuning knob)
         int ri = rpc;
         const char* ev = std::getenv("SRSB_RPC_INV");
-        if (ev && G == 1 && !c->slab) {
+        if (rm) {
+            ri = 64 / T_h > 1 ? 64 / T_h : 1;       // row-major: >= 64 threads per CTA (C3: 2 rows 0.146 ms, 1 row 0.158; C4 / C5: 1 row)
+            if (ri > Ml) ri = Ml;
+        }
+        if (ev && (G == 1 || rm) && !c->slab) {
             const int v = std::atoi(ev);
             if (v >= 2 && v <= Ml && v * T_h <= 512 && (v & (v - 1)) == 0) ri = v;
         }
@@ -324,6 +385,40 @@ sr_status configure(sr_sb_ctx* c) {
     {   // long contiguous columns (whole image, G = 1, M >= 4096): persistent prefetching solve
         const char* ev = std::getenv("SRSB_COLS_P");
         c->cols_p = (!c->slab && G == 1 && !(ev && ev[0] == '0')) ? pick_col_p(lgM, c->use_sym) : nullptr;
+    }
+    {   // cyclic tridiagonal column solve instead of FFT -> divide -> inverse FFT (sr_tri.cuh; SRSB_COLS_TRI=0: off)
+        const char* ev = std::getenv("SRSB_COLS_TRI");
+        const int L = 1 << kTriLogL;
+        c->cols_tri = nullptr;
+        if (!c->slab && G == 1 && M >= L && !(ev && ev[0] == '0')) {
+            const int C = M / L;                       // threads per column
+            int tcpc = 1;
+            int want = 128;   // threads per CTA (M <= 2048; one column needs M / 16): measured C3 0.0875 ms at 128, 0.0899 at 256, 0.105 at 512
+            if (const char* e2 = std::getenv("SRSB_TRI_THREADS")) want = std::atoi(e2);
+            while (tcpc * 2 * C <= want && tcpc * 2 <= H) tcpc *= 2;
+            if (tcpc * C <= 512) {
+                c->cols_tri = pick_col_tri();
+                c->tri_lg_cpc = ilog2(tcpc);
+                c->tri_threads = tcpc * C;
+                c->tri_smem = tcpc * (M + 3 * C) * (int)sizeof(float2);
+                c->tri_grid = dim3(H / tcpc, B, 1);
+            }
+        }
+    }
+    c->cols_tri_rm = nullptr;
+    if (rm) {
+        const int L = 1 << kTriLogL, C = M / L;
+        int W = 8;    // chunk warps per CTA (measured C3 0.093 ms at 8, 0.101 at 16; C5 0.095 / 0.107)
+        if (const char* e2 = std::getenv("SRSB_TRI_W")) W = std::atoi(e2);
+        if (W < 1 || !is_pow2(W) || W > 16) W = 16;
+        if (W > C) W = C;
+        c->cols_tri_rm = pick_col_tri_rm();
+        c->trm_mmax = rm_mmax;
+        c->trm_threads = 32 * W;
+        c->trm_smem = (W * L + 2 * (rm_mmax + W)) * 32 * (int)sizeof(float2);
+        c->trm_grid = dim3(H / 32, C / W, B);
+        if (!c->spec2 && cudaMalloc((void**)&c->spec2, (size_t)H * M * B * sizeof(float2)) != cudaSuccess)
+            return fail(c, SR_ERR_OOM, "spectrum allocation failed");
     }
     c->cgrid = dim3(Hl / cpc, B, 1);
     if (c->slab) {   // all-to-all chunks (column groups) pipelined with the column solve; SRSB_A2A_CHUNKS
@@ -441,6 +536,10 @@ sr_status configure(sr_sb_ctx* c) {
     CK(cudaFuncSetAttribute((const void*)c->rfwd, cudaFuncAttributeMaxDynamicSharedMemorySize, c->rsmem));
     CK(cudaFuncSetAttribute((const void*)c->rinv, cudaFuncAttributeMaxDynamicSharedMemorySize, c->rsmem_inv));
     CK(cudaFuncSetAttribute((const void*)c->cols, cudaFuncAttributeMaxDynamicSharedMemorySize, c->csmem));
+    if (c->cols_tri_rm)
+        CK(cudaFuncSetAttribute((const void*)c->cols_tri_rm, cudaFuncAttributeMaxDynamicSharedMemorySize, c->trm_smem));
+    if (c->cols_tri)
+        CK(cudaFuncSetAttribute((const void*)c->cols_tri, cudaFuncAttributeMaxDynamicSharedMemorySize, c->tri_smem));
     if (c->cols_p) {
         c->cp_threads = M / 16;
         c->cp_smem = (M + c->ca.SC) * (int)sizeof(float2) + 16;
@@ -489,6 +588,33 @@ sr_status make_tables(sr_sb_ctx* c) {
         CK(cudaMemcpyAsync(c->sym, sym.data(), sym.size() * sizeof(float), cudaMemcpyHostToDevice, c->s));
     }
     c->ca.sym = c->sym;
+    if (c->cols_tri || c->cols_tri_rm) {   // per-column constants of the cyclic tridiagonal solve, fp64 -> fp32 (sr_tri.cuh)
+        std::vector<TriCol> tab(H);
+        const double a = (double)c->p.tau * (double)c->p.mu;
+        const int L = 1 << kTriLogL, C = M / L;
+        auto fill = [&](TriCol& t, int comp, int k2, int& mmax) {
+            double sq = 1.0, clos = 1.0;
+            const double r = tri_ratio(a, 1.0 + a * (4.0 - 2.0 * std::cos(2 * pi * k2 / N)), &sq);
+            const double rho = std::pow(r, L);
+            const int m = tri_carry_terms(rho, C, &clos);
+            t.r[comp] = (float)r;
+            t.ks[comp] = (float)(1.0 / (sq * (double)H));
+            t.rho[comp] = (float)rho;
+            t.clos[comp] = (float)clos;
+            mmax = std::max(mmax, m);
+        };
+        for (int k2 = 0; k2 < H; k2++) {
+            int mm = 1;
+            fill(tab[k2], 0, k2, mm);
+            fill(tab[k2], 1, k2 == 0 ? H : k2, mm);   // slot 0: imaginary part = the real column k2 = N/2
+            tab[k2].mmax = mm;
+            tab[k2].pad_[0] = tab[k2].pad_[1] = tab[k2].pad_[2] = 0;
+        }
+        if (!c->tri_tab && cudaMalloc((void**)&c->tri_tab, H * sizeof(TriCol)) != cudaSuccess)
+            return fail(c, SR_ERR_OOM, "tridiagonal table allocation failed");
+        CK(cudaMemcpyAsync(c->tri_tab, tab.data(), H * sizeof(TriCol), cudaMemcpyHostToDevice, c->s));
+        CK(cudaStreamSynchronize(c->s));   // tab is a local
+    }
     if (c->p.phi_solver == SR_PHI_AOS) {   // LR factors once, fp64 -> fp32
         auto factors = [&](int n, std::vector<float>& cp, std::vector<float>& r) {
             const double cc = 2.0 * (double)c->p.tau * (double)c->p.mu, a = -cc;
@@ -542,7 +668,13 @@ void enq_r2c(sr_sb_ctx* c, const float* F) {
 }
 void enq_cols(sr_sb_ctx* c) {
     prof_begin(c);
-    if (c->cols_p)
+    if (c->cols_tri_rm)
+        c->cols_tri_rm<<<c->trm_grid, c->trm_threads, c->trm_smem, c->s>>>(c->spec, c->spec2, c->tri_tab, ilog2(c->p.M),
+                                                                           c->ca.lg_G, c->p.N / 2, c->trm_mmax);
+    else if (c->cols_tri)
+        c->cols_tri<<<c->tri_grid, c->tri_threads, c->tri_smem, c->s>>>(c->spec, c->tri_tab, ilog2(c->p.M), c->tri_lg_cpc,
+                                                                        ilog2(c->p.N / 2));
+    else if (c->cols_p)
         c->cols_p<<<c->cp_grid, c->cp_threads, c->cp_smem, c->s>>>(c->spec, c->twM, c->cM, c->cN, c->ca,
                                                                   c->p.batch * (c->p.N / 2), ilog2(c->p.N / 2));
     else
@@ -568,7 +700,7 @@ void enq_c2r(sr_sb_ctx* c, float* out, float clip, int accum, int sweep = -1) {
     ra.stats = mon ? c->mon_part + c->part_c2r + (size_t)sweep * c->rgrid_inv.x * c->p.batch * 2 : nullptr;
     ra.stats_stride = c->stats_stride;
     prof_begin(c);
-    c->rinv<<<c->rgrid_inv, c->rblock_inv, c->rsmem_inv, c->s>>>(c->spec, out, c->twH, c->twR, ra);
+    c->rinv<<<c->rgrid_inv, c->rblock_inv, c->rsmem_inv, c->s>>>(c->cols_tri_rm ? c->spec2 : c->spec, out, c->twH, c->twR, ra);
     prof_end(c, SR_K_ROWS_C2R);
     if (mon)   // ||phi^{s+1} - phi^s||^2, ||phi^s||^2 per image, summed in a fixed order
         k_reduce_partials<<<c->p.batch * 2, 32, 0, c->s>>>(ra.stats, (int)c->rgrid_inv.x, 2, c->stats + 4 + 2 * sweep,
@@ -1509,7 +1641,7 @@ void sr_sb_destroy(sr_sb_ctx* c) {
     drop_graphs(c);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     void* ptrs[] = {c->phi_base, c->F_base, c->w_base[0], c->w_base[1], c->b_base, c->g_base, c->spec,
-                    c->spec_cols, c->twH, c->twM, c->twR, c->cM, c->cN, c->sym, c->flag, c->stats, c->prev_phi, c->conv, c->mon_part,
+                    c->spec_cols, c->twH, c->twM, c->twR, c->cM, c->cN, c->sym, c->tri_tab, c->spec2, c->flag, c->stats, c->prev_phi, c->conv, c->mon_part,
                     c->aos_cpM, c->aos_rM, c->aos_cpN, c->aos_rN};
     for (void* q : ptrs)
         if (q) cudaFree(q);

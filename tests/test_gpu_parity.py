@@ -49,11 +49,21 @@ def _periodic_residual(phi, F, tau, mu):
     return np.linalg.norm(phi - tau * mu * lap - F) / np.linalg.norm(F)
 
 
+def _cols_env(monkeypatch, cols):
+    """Column pass of the solve: 'rm' = cyclic tridiagonal solve on the row-major spectrum (the default where
+    N >= 64, M >= 16 and the carries are short), 'tri' = the same on the transposed spectrum (contiguous
+    columns), 'fft' = FFT -> divide by the symbol -> inverse FFT."""
+    monkeypatch.setenv("SRSB_COLS_TRI", "0" if cols == "fft" else "1")
+    monkeypatch.setenv("SRSB_SPEC_RM", "1" if cols == "rm" else "0")
+
+
 # ----------------------------------------------------------------------------- FFT solve, Eq. (33)
 @pytest.mark.parametrize("M,N,batch", [(8, 8, 1), (16, 64, 2), (64, 16, 1), (128, 128, 1), (32, 512, 1),
                                        (512, 32, 1), (256, 256, 3), (1024, 1024, 2), (2048, 256, 1),
                                        (256, 4096, 1), (8192, 16, 1), (16, 8192, 1)])
-def test_solve_parity(S, orc, M, N, batch):
+@pytest.mark.parametrize("cols", ["rm", "tri", "fft"])
+def test_solve_parity(S, orc, M, N, batch, cols, monkeypatch):
+    _cols_env(monkeypatch, cols)
     p = _params(3)
     rng = np.random.default_rng(M * 7 + N)
     F = rng.standard_normal((batch, M, N)).astype(np.float32)
@@ -66,9 +76,35 @@ def test_solve_parity(S, orc, M, N, batch):
         assert _periodic_residual(out[b], F[b].astype(np.float64), p["tau"], p["mu"]) < 2e-6
 
 
-def test_solve_closed_forms(S):
+@pytest.mark.parametrize("M,N,tau,mu", [(16, 64, 0.05, 8.0), (16, 16, 5.0, 8.0), (64, 64, 5.0, 20.0),
+                                        (1024, 256, 1.0, 8.0), (1024, 1024, 30.0, 8.0), (4096, 64, 0.5, 8.0),
+                                        (256, 256, 0.0, 8.0), (128, 128, 1e-4, 1.0), (512, 128, 0.25, 8.0),
+                                        (64, 128, 0.3, 8.0)])
+@pytest.mark.parametrize("cols", ["rm", "tri"])
+def test_solve_tridiagonal_column_pass_any_stiffness(S, orc, M, N, tau, mu, cols, monkeypatch):
+    """sr_tri.cuh: the carry sum of the chunked recurrences must hold from r = 0 (tau = 0) to r -> 1
+    (tau mu = 240: r = 0.94, carries that wrap around the whole column; the row-major kernel takes up to
+    4 carry terms and hands stiffer cases to the transposed one)."""
+    _cols_env(monkeypatch, cols)
+    p = _params(3, tau=tau, mu=mu)
+    rng = np.random.default_rng(M * 11 + N)
+    F = rng.standard_normal((2, M, N)).astype(np.float32)
+    F[1] = 0.0
+    F[1, M // 3, N // 5] = 1.0          # an impulse: the Green's function itself, wrap included
+    with _solver(S, M, N, 2, p) as sv:
+        out = _np(sv.debug_solve(_cuda(F)))
+    for b in range(2):
+        ref = orc.solve(F[b], tau, mu)
+        assert np.max(np.abs(out[b] - ref)) <= 1e-5 * np.max(np.abs(F[b])), b
+        # fp32 rounding of phi seen through A: up to (1 + 8 tau mu) eps |phi|
+        assert _periodic_residual(out[b], F[b].astype(np.float64), tau, mu) < 2e-6 * (1 + 8 * tau * mu)
+
+
+@pytest.mark.parametrize("cols", ["rm", "tri", "fft"])
+def test_solve_closed_forms(S, cols, monkeypatch):
     """Constant -> same constant; a single cos mode (k1, k2), including the packed k2 = 0 and
     k2 = N/2 columns, -> scaled by 1/symbol (Eq. 32)."""
+    _cols_env(monkeypatch, cols)
     M, N = 64, 128
     tau, mu = _params(3)["tau"], _params(3)["mu"]
     ii, jj = np.meshgrid(np.arange(M), np.arange(N), indexing="ij")
@@ -511,6 +547,7 @@ def test_launch_shape_instances_bitwise(S, M, N, env, monkeypatch):
     paired 16-byte transposed accesses) and the contiguous-column solve give bitwise the same Eq. (33)
     solve as the generic kernels: other shapes / layouts are forced with the tuning knobs (read at
     context creation), the butterflies and per-element arithmetic are identical."""
+    monkeypatch.setenv("SRSB_COLS_TRI", "0")   # FFT column pass on both sides (the knobs move G off 1)
     p = _params(4)
     F = np.random.default_rng(7).standard_normal((2, M, N)).astype(np.float32)
     with _solver(S, M, N, 2, p) as sv:

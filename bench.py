@@ -32,7 +32,8 @@ UNIT = "Mpx-iter/s"
 # algorithmic HBM bytes per pixel per launch of each kernel class
 BYTES_PER_PX = {"rhs": 28.0, "rows_r2c": 8.0, "cols_solve": 8.0, "rows_c2r": 12.0, "wb": 40.0,
                 "aos_vert": 8.0, "aos_horiz": 12.0,   # aos_vert: register-chunk kernel (M <= 2048)
-                "rhs_r2c": 28.0}   # fused RHS + row R2C: phi, w1, w2, b1, b2, g in, packed half spectrum out
+                "rhs_r2c": 28.0,   # fused RHS + row R2C: phi, w1, w2, b1, b2, g in, packed half spectrum out
+                "solve_cluster": 12.0}   # small images, one-kernel solve: D and psi in, phi out (the spectrum stays on chip)
 MODEL_BYTES_PER_PX_ITER = 172.0   # SURVEY.md §8(d) fused model (S = 3)
 
 

@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define SRSB_ABI_VERSION 2   /* 2: SR_K_RHS_R2C (SR_K_NCLASSES 7 -> 8) */
+#define SRSB_ABI_VERSION 3   /* 2: SR_K_RHS_R2C (SR_K_NCLASSES 7 -> 8); 3: SR_K_SOLVE_CLUSTER (8 -> 9) */
 
 typedef enum {
     SR_OK = 0,
@@ -175,7 +175,9 @@ typedef enum { SR_K_RHS = 0, SR_K_ROWS_R2C = 1, SR_K_COLS_SOLVE = 2, SR_K_ROWS_C
                SR_K_AOS_VERT = 5, SR_K_AOS_HORIZ = 6,   /* phi_solver = SR_PHI_AOS replaces classes 1-3 */
                SR_K_RHS_R2C = 7,   /* the fused RHS (Eq. 37) + row R2C cluster kernel: replaces classes 0-1 for
                                       whole-image FFT contexts with 128 <= N <= 1024 */
-               SR_K_NCLASSES = 8 } sr_kernel_class;
+               SR_K_SOLVE_CLUSTER = 8,   /* small images (M <= 512, 128 <= N <= 512): the whole solve of Eq. (31)-(33) in one
+                                            thread-block-cluster kernel, replaces classes 1-3 */
+               SR_K_NCLASSES = 9 } sr_kernel_class;
 
 /* Diagnostics: run K outer iterations WITHOUT the CUDA graph, bracketing every launch with CUDA
  * events on the context's work stream, and return per kernel class (sr_kernel_class) the summed

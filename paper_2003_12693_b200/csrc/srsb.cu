@@ -22,6 +22,7 @@
 #include "../../include/srsb.h"
 #include "sr_kernels.h"
 #include "sr_tri.cuh"
+#include "sr_solve_cl.cuh"
 #include <cudaTypedefs.h>
 #include "sr_setup.cuh"
 #include "sr_aos.cuh"
@@ -89,6 +90,10 @@ struct sr_sb_ctx {
     int cp_grid = 0, cp_smem = 0, cp_threads = 0;
     ColTriKernel cols_tri = nullptr;   // cyclic tridiagonal column solve (sr_tri.cuh): whole image, G = 1, M >= 16
     TriCol* tri_tab = nullptr;         // [H] per-column constants
+    SolveClKernel solve_cl = nullptr;  // small images: the whole solve in one cluster kernel (sr_solve_cl.cuh)
+    TriCol* tri_tab_cl = nullptr;      // its per-column constants (chunk length = rows per CTA)
+    SolveClArgs scl{};
+    int scl_nc = 0, scl_threads = 0, scl_smem = 0, scl_lg_rpc = 0;
     ColTriRmKernel cols_tri_rm = nullptr;   // the same on a row-major spectrum (G = N/2), spec -> spec2
     float2* spec2 = nullptr;           // row-major mode: the solved spectrum (k_cols_tri_rm is out of place)
     dim3 trm_grid;
@@ -420,6 +425,52 @@ sr_status configure(sr_sb_ctx* c) {
         if (!c->spec2 && cudaMalloc((void**)&c->spec2, (size_t)H * M * B * sizeof(float2)) != cudaSuccess)
             return fail(c, SR_ERR_OOM, "spectrum allocation failed");
     }
+    c->solve_cl = nullptr;
+    {   // small-image latency path: r2c + column solve + c2r in one cluster kernel (sr_solve_cl.cuh).  Default only for
+        // images up to 128 x 128 (C1: 346 -> 379 Mpx-iter/s); a cluster is at most 16 CTAs, so larger images lose more
+        // from running on 16 SMs than they gain from two launches fewer (C2 512^2: 5.1k -> 4.3k).  SRSB_SOLVE_CL=1 (or 5:
+        // 32 rows per CTA) forces it wherever it applies (M <= 512, 128 <= N <= 512), 0 turns it off.
+        const char* ev = std::getenv("SRSB_SOLVE_CL");
+        const char* et = std::getenv("SRSB_COLS_TRI");
+        const bool want = ev ? ev[0] != '0' : (M <= 128 && N <= 128);
+        if (!c->slab && p.phi_solver == SR_PHI_FFT && want && !(et && et[0] == '0') && M >= 16 && M <= 512 &&
+            H >= 64 && H <= 256) {
+            int lr = M / 16 <= 16 ? 4 : 5;
+            if (ev && ev[0] == '5' && M >= 32) lr = 5;
+            const int nc = M >> lr, nt = (H / 16) << lr;
+            SolveClKernel k = (nc >= 1 && nc <= 16 && nt >= H && nt <= 1024) ? pick_solve_cluster(lgH, lr) : nullptr;
+            if (k) {
+                const int SR = padded(H, 1);
+                const int smem_b = ((1 << lr) * SR + 2 * H) * (int)sizeof(float2);
+                bool ok = cudaFuncSetAttribute((const void*)k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_b) == cudaSuccess;
+                if (ok && nc > 8)
+                    ok = cudaFuncSetAttribute((const void*)k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+                cudaLaunchConfig_t cfg = {};
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeClusterDimension;
+                at[0].val.clusterDim.x = nc;
+                at[0].val.clusterDim.y = 1;
+                at[0].val.clusterDim.z = 1;
+                cfg.gridDim = dim3(nc, B, 1);
+                cfg.blockDim = dim3(nt, 1, 1);
+                cfg.dynamicSmemBytes = smem_b;
+                cfg.attrs = at;
+                cfg.numAttrs = 1;
+                int ncl = 0;
+                if (ok && cudaOccupancyMaxActiveClusters(&ncl, (const void*)k, &cfg) == cudaSuccess && ncl > 0) {
+                    c->solve_cl = k;
+                    c->scl_nc = nc;
+                    c->scl_threads = nt;
+                    c->scl_smem = smem_b;
+                    c->scl_lg_rpc = lr;
+                    c->scl.plane = c->pitch;
+                    c->scl.SR = SR;
+                } else {
+                    cudaGetLastError();
+                }
+            }
+        }
+    }
     c->cgrid = dim3(Hl / cpc, B, 1);
     if (c->slab) {   // all-to-all chunks (column groups) pipelined with the column solve; SRSB_A2A_CHUNKS
         int nk = 4;
@@ -588,10 +639,11 @@ sr_status make_tables(sr_sb_ctx* c) {
         CK(cudaMemcpyAsync(c->sym, sym.data(), sym.size() * sizeof(float), cudaMemcpyHostToDevice, c->s));
     }
     c->ca.sym = c->sym;
-    if (c->cols_tri || c->cols_tri_rm) {   // per-column constants of the cyclic tridiagonal solve, fp64 -> fp32 (sr_tri.cuh)
+    // per-column constants of the cyclic tridiagonal solve for chunk length L (C chunks per column), fp64 -> fp32
+    auto tri_table = [&](int L, int C, TriCol** dst, int* mmax_out) -> sr_status {
         std::vector<TriCol> tab(H);
         const double a = (double)c->p.tau * (double)c->p.mu;
-        const int L = 1 << kTriLogL, C = M / L;
+        int mall = 1;
         auto fill = [&](TriCol& t, int comp, int k2, int& mmax) {
             double sq = 1.0, clos = 1.0;
             const double r = tri_ratio(a, 1.0 + a * (4.0 - 2.0 * std::cos(2 * pi * k2 / N)), &sq);
@@ -609,12 +661,17 @@ sr_status make_tables(sr_sb_ctx* c) {
             fill(tab[k2], 1, k2 == 0 ? H : k2, mm);   // slot 0: imaginary part = the real column k2 = N/2
             tab[k2].mmax = mm;
             tab[k2].pad_[0] = tab[k2].pad_[1] = tab[k2].pad_[2] = 0;
+            mall = std::max(mall, mm);
         }
-        if (!c->tri_tab && cudaMalloc((void**)&c->tri_tab, H * sizeof(TriCol)) != cudaSuccess)
+        if (!*dst && cudaMalloc((void**)dst, H * sizeof(TriCol)) != cudaSuccess)
             return fail(c, SR_ERR_OOM, "tridiagonal table allocation failed");
-        CK(cudaMemcpyAsync(c->tri_tab, tab.data(), H * sizeof(TriCol), cudaMemcpyHostToDevice, c->s));
+        CK(cudaMemcpyAsync(*dst, tab.data(), H * sizeof(TriCol), cudaMemcpyHostToDevice, c->s));
         CK(cudaStreamSynchronize(c->s));   // tab is a local
-    }
+        if (mmax_out) *mmax_out = mall;
+        return SR_OK;
+    };
+    if (c->cols_tri || c->cols_tri_rm) RET(tri_table(1 << kTriLogL, M >> kTriLogL, &c->tri_tab, nullptr));
+    if (c->solve_cl) RET(tri_table(1 << c->scl_lg_rpc, c->scl_nc, &c->tri_tab_cl, &c->scl.mmax));
     if (c->p.phi_solver == SR_PHI_AOS) {   // LR factors once, fp64 -> fp32
         auto factors = [&](int n, std::vector<float>& cp, std::vector<float>& r) {
             const double cc = 2.0 * (double)c->p.tau * (double)c->p.mu, a = -cc;
@@ -705,6 +762,35 @@ void enq_c2r(sr_sb_ctx* c, float* out, float clip, int accum, int sweep = -1) {
     if (mon)   // ||phi^{s+1} - phi^s||^2, ||phi^s||^2 per image, summed in a fixed order
         k_reduce_partials<<<c->p.batch * 2, 32, 0, c->s>>>(ra.stats, (int)c->rgrid_inv.x, 2, c->stats + 4 + 2 * sweep,
                                                            c->stats_stride);
+}
+// the phi solve of one sweep: F -> out (+= when accum), clamped when clip > 0.  Small images: one cluster kernel
+// (not with the NEXT-1 monitor, whose per-sweep sums live in the c2r pass)
+void enq_solve(sr_sb_ctx* c, const float* F, float* out, float clip, int accum, int sweep = -1) {
+    if (c->solve_cl && !(c->stats && sweep >= 0)) {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = c->scl_nc;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(c->scl_nc, c->p.batch, 1);
+        cfg.blockDim = dim3(c->scl_threads, 1, 1);
+        cfg.dynamicSmemBytes = c->scl_smem;
+        cfg.stream = c->s;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        SolveClArgs a = c->scl;
+        a.clip = clip;
+        a.accum = accum;
+        prof_begin(c);
+        cudaLaunchKernelEx(&cfg, c->solve_cl, F, out, (const float2*)c->twH, (const float2*)c->twR,
+                           (const TriCol*)c->tri_tab_cl, a);
+        prof_end(c, SR_K_SOLVE_CLUSTER);
+        return;
+    }
+    enq_r2c(c, F);
+    enq_cols(c);
+    enq_c2r(c, out, clip, accum, sweep);
 }
 void enq_rhs(sr_sb_ctx* c, float* F) {
     prof_begin(c);
@@ -931,9 +1017,7 @@ sr_status enq_iteration(sr_sb_ctx* c) {   // whole-image context
         if (c->p.phi_solver == SR_PHI_AOS) {
             enq_aos(c, c->F, c->phi, clip);
         } else {
-            enq_r2c(c, c->F);
-            enq_cols(c);
-            enq_c2r(c, c->phi, clip, 1, s);
+            enq_solve(c, c->F, c->phi, clip, 1, s);
         }
     }
     const int passes = c->p.w_mode == SR_W_FIXED_POINT ? c->p.w_iters : 1;
@@ -1485,9 +1569,7 @@ sr_status sr_sb_debug_solve(sr_sb_ctx* c, const float* F, float* phi_out) {
         RET(copy_planes(c, c->F, phi_out, c->p.batch, false));
     } else {
         float* tmp = c->w[c->wcur ^ 1];
-        enq_r2c(c, c->F);
-        enq_cols(c);
-        enq_c2r(c, tmp, 0.f, 0);
+        enq_solve(c, c->F, tmp, 0.f, 0);
         RET(copy_planes(c, tmp, phi_out, c->p.batch, false));
     }
     RET(end(c));
@@ -1625,8 +1707,8 @@ double sr_sb_last_change(const sr_sb_ctx* c) { return c ? c->last_change : -1.0;
 
 int sr_sb_launches_per_iteration(const sr_sb_ctx* c) {
     if (!c) return -1;
-    // rhs + (r2c, cols, c2r | vert, horiz); fused: rhs_r2c, cols, c2r
-    const int per_sweep = (c->p.phi_solver == SR_PHI_AOS || c->rhs_r2c) ? 3 : 4;
+    // rhs + (r2c, cols, c2r | vert, horiz | the one-kernel cluster solve); fused: rhs_r2c, cols, c2r
+    const int per_sweep = (c->p.phi_solver == SR_PHI_AOS || c->rhs_r2c) ? 3 : (c->solve_cl && !c->stats) ? 2 : 4;
     const int per = per_sweep * c->p.S + (c->p.w_mode == SR_W_FIXED_POINT ? c->p.w_iters : 1);
     return c->backend == BK_LOCAL ? per * (int)c->members.size() : per;
 }
@@ -1641,7 +1723,7 @@ void sr_sb_destroy(sr_sb_ctx* c) {
     drop_graphs(c);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     void* ptrs[] = {c->phi_base, c->F_base, c->w_base[0], c->w_base[1], c->b_base, c->g_base, c->spec,
-                    c->spec_cols, c->twH, c->twM, c->twR, c->cM, c->cN, c->sym, c->tri_tab, c->spec2, c->flag, c->stats, c->prev_phi, c->conv, c->mon_part,
+                    c->spec_cols, c->twH, c->twM, c->twR, c->cM, c->cN, c->sym, c->tri_tab, c->tri_tab_cl, c->spec2, c->flag, c->stats, c->prev_phi, c->conv, c->mon_part,
                     c->aos_cpM, c->aos_rM, c->aos_cpN, c->aos_rN};
     for (void* q : ptrs)
         if (q) cudaFree(q);

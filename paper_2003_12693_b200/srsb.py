@@ -33,7 +33,7 @@ EXPORTS = ["sr_sb_default_params", "sr_sb_create", "sr_sb_set_image", "sr_sb_ite
            "sr_sb3_set_state", "sr_sb3_debug_solve", "sr_sb3_debug_rhs", "sr_sb3_profile", "sr_sb3_sync",
            "sr_sb3_destroy", "sr_sb3_last_error"]
 KERNEL_CLASSES = ["rhs", "rows_r2c", "cols_solve", "rows_c2r", "wb", "aos_vert", "aos_horiz",
-                  "rhs_r2c"]   # sr_kernel_class
+                  "rhs_r2c", "solve_cluster"]   # sr_kernel_class
 
 
 class SrsbError(RuntimeError):

@@ -30,7 +30,7 @@ def test_every_declared_symbol_is_exported(srsb):
     for n in names:
         assert hasattr(L, n), n
     assert sorted(srsb.EXPORTS) == names
-    assert L.sr_sb_abi_version() == 2
+    assert L.sr_sb_abi_version() == 3
 
 
 def test_library_is_sm100a_only(srsb):

@@ -24,6 +24,15 @@ def S():
     return srsb
 
 
+@pytest.fixture(autouse=True)
+def _fft_column_pass(monkeypatch):
+    """Slab contexts run the column pass as FFT -> divide -> inverse FFT on the all-to-all-transposed
+    spectrum; whole-image contexts default to the cyclic tridiagonal column pass (another rounding order of
+    the same solve).  The bitwise slab == whole-image property is a statement about identical butterflies,
+    so the whole-image side runs the FFT column pass here too (knob read at context creation)."""
+    monkeypatch.setenv("SRSB_COLS_TRI", "0")
+
+
 KEYS = ("gamma", "alpha", "beta", "mu", "epsilon", "l", "d", "window_shape", "tau", "S", "rho", "sigma", "s",
         "phi_clip", "w_proj", "w_mode", "w_iters")
 

@@ -6,7 +6,7 @@ import json
 import subprocess
 import sys
 
-CLASSES = [("k_rhs_r2c", "rhs_r2c"), ("k_rhs", "rhs"), ("k_wb", "wb"), ("k_rows_r2c", "rows_r2c"), ("k_cols_solve", "cols_solve"),
+CLASSES = [("k_rhs_r2c", "rhs_r2c"), ("k_rhs", "rhs"), ("k_wb", "wb"), ("k_rows_r2c", "rows_r2c"), ("k_cols_solve", "cols_solve"), ("k_cols_tri", "cols_solve"),
            ("k_rows_c2r", "rows_c2r"), ("k_aos_vert", "aos_vert"), ("k_aos_horiz", "aos_horiz")]
 
 

@@ -133,6 +133,19 @@ int sr_sb_slab_schedule(int kind, int P, int r, int Ml, int gh, int N, int k, in
  * SRSB_A2A_CHUNKS overrides the default 4 at creation). */
 int sr_sb_a2a_chunks(const sr_sb_ctx* ctx);
 
+/* Host logic of the tridiagonal column pass (needs no GPU).  After the row FFT, Eq. (31)-(33)
+ * (symbol of Eq. 32 as read in Q10) leave per spectrum column k2 in [0, N/2] the cyclic system
+ *   c x_i - a (x_{i-1} + x_{i+1}) = d_i,   a = tau mu,  c = 1 + tau mu (4 - 2 cos(2 pi k2 / N)),
+ * solved by two first-order recurrences cut into C chunks of L elements.  Writes the constants the kernels
+ * use, exactly as the context tabulates them (fp64):
+ *   out[0] = r = 2a / (c + sqrt(c^2 - 4 a^2))     recurrence ratio
+ *   out[1] = kappa = 1 / sqrt(c^2 - 4 a^2)        Green's function scale (the kernels fold 2/N into it)
+ *   out[2] = rho = r^L                            chunk-to-chunk carry ratio
+ *   out[3] = closure factor 1 / (1 - rho^C) if the carry sum runs a full wrap of the column, else 1
+ *   out[4] = carry terms mmax in [1, C]: the smallest m with rho^m < 2^-48
+ * Returns 0, or -1 on bad arguments (N >= 2, 0 <= k2 <= N/2, L >= 1, C >= 1, tau >= 0, mu > 0). */
+int sr_sb_tri_constants(float tau, float mu, int N, int k2, int L, int C, double* out);
+
 /* Algorithm 1 step (1): image f and initial level set phi0 ([batch][M][N]) ->
  * g (Eq. 1), phi = phi0, w = grad phi0 (Q12), b = 0.  Resets k to 0. */
 sr_status sr_sb_set_image(sr_sb_ctx* ctx, const float* image, const float* phi0);

@@ -1759,6 +1759,21 @@ int sr_sb_slab_schedule(int kind, int P, int r, int Ml, int gh, int N, int k, in
     return (int)ops.size();
 }
 
+int sr_sb_tri_constants(float tau, float mu, int N, int k2, int L, int C, double* out) {
+    if (!out || N < 2 || k2 < 0 || k2 > N / 2 || L < 1 || C < 1 || !(tau >= 0.f) || !(mu > 0.f)) return -1;
+    const double a = (double)tau * (double)mu;
+    double sq = 1.0, clos = 1.0;
+    const double r = tri_ratio(a, 1.0 + a * (4.0 - 2.0 * std::cos(2 * 3.14159265358979323846 * k2 / N)), &sq);
+    const double rho = std::pow(r, L);
+    const int m = tri_carry_terms(rho, C, &clos);
+    out[0] = r;
+    out[1] = 1.0 / sq;
+    out[2] = rho;
+    out[3] = clos;
+    out[4] = (double)m;
+    return 0;
+}
+
 int sr_sb_a2a_chunks(const sr_sb_ctx* c) { return c ? (c->backend == BK_LOCAL ? c->members[0]->a2a_chunks : c->a2a_chunks) : -1; }
 
 }  // extern "C"

@@ -28,7 +28,7 @@ EXPORTS = ["sr_sb_default_params", "sr_sb_create", "sr_sb_set_image", "sr_sb_ite
            "sr_sb_last_error", "sr_sb_abi_version", "sr_sb_profile", "sr_sb_create_slab_group",
            "sr_sb_nccl_unique_id", "sr_sb_create_slab_nccl", "sr_sb_local_rows", "sr_sb_set_monitor",
            "sr_sb_get_monitor", "sr_sb_iterate_until", "sr_sb_last_change", "sr_sb_create_dist", "sr_sb_set_iteration",
-           "sr_sb_slab_schedule", "sr_sb_a2a_chunks",
+           "sr_sb_slab_schedule", "sr_sb_a2a_chunks", "sr_sb_tri_constants",
            "sr_sb3_create", "sr_sb3_set_image", "sr_sb3_iterate", "sr_sb3_get_phi", "sr_sb3_get_state",
            "sr_sb3_set_state", "sr_sb3_debug_solve", "sr_sb3_debug_rhs", "sr_sb3_profile", "sr_sb3_sync",
            "sr_sb3_destroy", "sr_sb3_last_error"]
@@ -93,6 +93,7 @@ def lib():
             "sr_sb_set_iteration": (st, [p, C.c_longlong]),
             "sr_sb_slab_schedule": (i, [i, i, i, i, i, i, i, i, C.POINTER(C.c_longlong), i]),
             "sr_sb_a2a_chunks": (i, [p]),
+            "sr_sb_tri_constants": (i, [C.c_float, C.c_float, i, i, i, i, C.POINTER(C.c_double)]),
             "sr_sb3_create": (st, [C.POINTER(Params), i, i, p, C.POINTER(p)]),
             "sr_sb3_set_image": (st, [p, p, p]),
             "sr_sb3_iterate": (st, [p, i]),
@@ -131,6 +132,14 @@ def slab_schedule(kind, P, r, Ml, gh, N, k=0, nk=1):
     buf = (C.c_longlong * (5 * max(n, 1)))()
     lib().sr_sb_slab_schedule(kind, P, r, Ml, gh, N, k, nk, buf, n)
     return [tuple(int(buf[5 * i + j]) for j in range(5)) for i in range(n)]
+
+
+def tri_constants(tau, mu, N, k2, L, C_chunks):
+    """sr_sb_tri_constants: (r, kappa, rho, closure, mmax) of spectrum column k2 for chunks of L (host logic)."""
+    out = (C.c_double * 5)()
+    if lib().sr_sb_tri_constants(float(tau), float(mu), int(N), int(k2), int(L), int(C_chunks), out) != 0:
+        raise SrsbError(SR_ERR_ARG, "bad tridiagonal-constants arguments")
+    return float(out[0]), float(out[1]), float(out[2]), float(out[3]), int(out[4])
 
 
 def default_params(M, N, batch=1, window=4) -> dict:

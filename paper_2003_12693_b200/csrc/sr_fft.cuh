@@ -563,6 +563,10 @@ static __device__ __noinline__ void c2r_partials(float dsum, float osum, double*
                             // Measured on C3: 0.258 ms per launch (78 registers, 3 CTAs / SM) against 0.189 ms
                             // with psi in registers (128 registers, 2 CTAs / SM): off
 #endif
+#ifndef SRSB_C2R_OWN_PF
+#define SRSB_C2R_OWN_PF 0   // 1: L2 bulk prefetch of the CTA's own psi rows at its start (with SRSB_C2R_LATE_OLD=1: the
+                            // accumulation source is then loaded after the FFT, 32 registers fewer across it)
+#endif
 template <int LOGH, int LOGE, int LRPC = -1, int LG = -1>
 __global__ void __launch_bounds__(LRPC >= 0 ? ((H_OF(LOGH) / (1 << LOGE)) << (LRPC >= 0 ? LRPC : 0)) : 512,
                                   (LRPC >= 0 && ((H_OF(LOGH) / (1 << LOGE)) << (LRPC >= 0 ? LRPC : 0)) <= 256) ? SRSB_C2R_MINB
@@ -587,6 +591,7 @@ k_rows_c2r(const float2* __restrict__ spec, float* __restrict__ phi,
         if (block_ahead_2d(SRSB_C2R_PF_DIST, bx, by))
             bulk_prefetch_l2(phi + by * a.plane + (long long)(bx * rpc) * (2 * H), (uint32_t)(rpc * 2 * H * 4));
     }
+    if (SRSB_C2R_OWN_PF && a.accum && t == 0) bulk_prefetch_l2(out, (uint32_t)(2 * H * 4));
     // accumulation source (phi of the previous sweep), fetched first: its latency hides behind the FFT.
     // OSM: into shared memory by cp.async (no registers held across the FFT), else into registers
     constexpr bool OSM = SRSB_C2R_OLD_SMEM && LRPC >= 0 && !SRSB_C2R_LATE_OLD;

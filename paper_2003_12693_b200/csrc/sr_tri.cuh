@@ -40,11 +40,15 @@ struct TriCol {       // per global spectrum column k2; [0] real part, [1] imagi
 #define SRSB_TRI_MINB 2
 #endif
 
-// spec: [B][H][M] complex (G = 1: each column contiguous), solved in place.  grid (H / cpc, B),
+// spec: [B][H][M] complex (G = 1: each column contiguous), solved in place.  grid (columns / cpc, B),
 // block cpc * M / L threads, dynamic shared memory cpc * (M + 3 M / L) float2.
+// Slab mode: the all-to-all receive buffer holds column k2l as P segments of 2^lg_seg rows,
+// segment s at s * seg_stride + (k2l << lg_seg) (whole image: one segment, lg_seg = lgM); tc points at the
+// entry of local column 0 (global column k2_off).  Same chunks, same sums: bitwise the whole-image result.
 template <int LOGL>
 __global__ void __launch_bounds__(512, SRSB_TRI_MINB) k_cols_tri(float2* __restrict__ spec, const TriCol* __restrict__ tc,
-                                                                 int lgM, int lg_cpc, int lgH) {
+                                                                 int lgM, int lg_cpc, long long bstride, int lg_seg,
+                                                                 long long seg_stride) {
     constexpr int L = 1 << LOGL;
     extern __shared__ float2 smem2[];
     const int M = 1 << lgM, lgC = lgM - LOGL, C = 1 << lgC;
@@ -55,15 +59,20 @@ __global__ void __launch_bounds__(512, SRSB_TRI_MINB) k_cols_tri(float2* __restr
     float2* data = smem2;                          // [cpc][SC]
     float2* Bf = smem2 + cpc * SC;                 // [cpc][C]
     float2* Bb = Bf + cpc * C;
-    float2* g = spec + ((((size_t)blockIdx.y << lgH) + ((size_t)blockIdx.x << lg_cpc)) << lgM);
-    // stage the CTA's cpc contiguous columns (coalesced 8-byte cp.async into the padded rows)
+    float2* g = spec + blockIdx.y * bstride + ((long long)(blockIdx.x << lg_cpc) << lg_seg);
+    const int segmask = (1 << lg_seg) - 1;
+    // element i of the CTA's column cl
+    auto at = [&](int cl, int i) -> float2* {
+        return g + (long long)(i >> lg_seg) * seg_stride + ((long long)cl << lg_seg) + (i & segmask);
+    };
+    // stage the CTA's cpc columns (coalesced 8-byte cp.async into the padded rows)
 #pragma unroll 4
     for (int u = 0; u < L; u++) {
         const int e = tid + u * T;
         const int cl = e >> lgM, i = e & (M - 1);
         float2* dst = data + cl * SC + i + (i >> LOGL);
         SRSB_CHK(dst, 8);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(g + e) : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(at(cl, i)) : "memory");
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
     const int cl = tid >> lgC, c = tid & (C - 1);
@@ -130,7 +139,7 @@ __global__ void __launch_bounds__(512, SRSB_TRI_MINB) k_cols_tri(float2* __restr
     for (int u = 0; u < L; u++) {
         const int e = tid + u * T;
         const int cl2 = e >> lgM, i = e & (M - 1);
-        g[e] = data[cl2 * SC + i + (i >> LOGL)];
+        *at(cl2, i) = data[cl2 * SC + i + (i >> LOGL)];
     }
 }
 
@@ -244,7 +253,7 @@ __global__ void __launch_bounds__(512, 2) k_cols_tri_rm(const float2* __restrict
     }
 }
 
-typedef void (*ColTriKernel)(float2*, const TriCol*, int, int, int);
+typedef void (*ColTriKernel)(float2*, const TriCol*, int, int, long long, int, long long);
 typedef void (*ColTriRmKernel)(const float2*, float2*, const TriCol*, int, int, int, int);
 ColTriRmKernel pick_col_tri_rm();   // fft_tri.cu
 ColTriKernel pick_col_tri();     // fft_tri.cu

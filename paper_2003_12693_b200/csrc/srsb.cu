@@ -274,6 +274,8 @@ sr_status configure(sr_sb_ctx* c) {
     if (G < 1) G = 1;
     if (M >= 4096 && !c->slab) G = 1;   // long columns: contiguous, so the column solve reads whole sectors
                                         // and can prefetch a column with one bulk copy (C5 +1.7 %; C4 14.46k -> 14.86k)
+    const bool tri_on = !(std::getenv("SRSB_COLS_TRI") && std::getenv("SRSB_COLS_TRI")[0] == '0');
+    if (c->slab && tri_on && p.phi_solver == SR_PHI_FFT) G = 1;   // the tridiagonal column pass wants contiguous column segments
     if (G > H / P) G = H / P;
     if (const char* ev = std::getenv("SRSB_G")) {     // tuning knob (power of two)
         const int v = std::atoi(ev);
@@ -395,18 +397,18 @@ sr_status configure(sr_sb_ctx* c) {
         const char* ev = std::getenv("SRSB_COLS_TRI");
         const int L = 1 << kTriLogL;
         c->cols_tri = nullptr;
-        if (!c->slab && G == 1 && M >= L && !(ev && ev[0] == '0')) {
+        if (G == 1 && M >= L && Ml >= L && !(ev && ev[0] == '0')) {   // slab: a chunk lies inside one segment (Ml >= L)
             const int C = M / L;                       // threads per column
             int tcpc = 1;
             int want = 128;   // threads per CTA (M <= 2048; one column needs M / 16): measured C3 0.0875 ms at 128, 0.0899 at 256, 0.105 at 512
             if (const char* e2 = std::getenv("SRSB_TRI_THREADS")) want = std::atoi(e2);
-            while (tcpc * 2 * C <= want && tcpc * 2 <= H) tcpc *= 2;
+            while (tcpc * 2 * C <= want && tcpc * 2 <= Hl) tcpc *= 2;
             if (tcpc * C <= 512) {
                 c->cols_tri = pick_col_tri();
                 c->tri_lg_cpc = ilog2(tcpc);
                 c->tri_threads = tcpc * C;
                 c->tri_smem = tcpc * (M + 3 * C) * (int)sizeof(float2);
-                c->tri_grid = dim3(H / tcpc, B, 1);
+                c->tri_grid = dim3(Hl / tcpc, B, 1);
             }
         }
     }
@@ -475,7 +477,7 @@ sr_status configure(sr_sb_ctx* c) {
     if (c->slab) {   // all-to-all chunks (column groups) pipelined with the column solve; SRSB_A2A_CHUNKS
         int nk = 4;
         if (const char* ev = std::getenv("SRSB_A2A_CHUNKS")) nk = std::atoi(ev);
-        const int unit = std::max(G, cpc);   // a chunk holds whole column groups and whole column CTAs
+        const int unit = std::max(std::max(G, cpc), c->cols_tri ? (1 << c->tri_lg_cpc) : 1);   // a chunk holds whole column groups and whole column CTAs
         while (nk > 1 && (!is_pow2(nk) || nk > sr_sb_ctx::kMaxChunks || Hl / nk < unit || (Hl / nk) % unit)) nk--;
         c->a2a_chunks = std::max(nk, 1);
     }
@@ -729,8 +731,10 @@ void enq_cols(sr_sb_ctx* c) {
         c->cols_tri_rm<<<c->trm_grid, c->trm_threads, c->trm_smem, c->s>>>(c->spec, c->spec2, c->tri_tab, ilog2(c->p.M),
                                                                            c->ca.lg_G, c->p.N / 2, c->trm_mmax);
     else if (c->cols_tri)
-        c->cols_tri<<<c->tri_grid, c->tri_threads, c->tri_smem, c->s>>>(c->spec, c->tri_tab, ilog2(c->p.M), c->tri_lg_cpc,
-                                                                        ilog2(c->p.N / 2));
+        c->cols_tri<<<c->tri_grid, c->tri_threads, c->tri_smem, c->s>>>(c->slab ? c->spec_cols : c->spec,
+                                                                        c->tri_tab + c->ca.k2_off, ilog2(c->p.M),
+                                                                        c->tri_lg_cpc, c->ca.bstride, c->ca.lg_seg,
+                                                                        c->ca.seg_stride);
     else if (c->cols_p)
         c->cols_p<<<c->cp_grid, c->cp_threads, c->cp_smem, c->s>>>(c->spec, c->twM, c->cM, c->cN, c->ca,
                                                                   c->p.batch * (c->p.N / 2), ilog2(c->p.N / 2));
@@ -745,8 +749,13 @@ void enq_cols_chunk(sr_sb_ctx* c, int k, int nk, cudaStream_t st) {
     FftColArgs ca = c->ca;
     ca.k2_off += k * Hk;
     prof_begin(c);
-    c->cols<<<dim3(Hk >> ca.lg_cpc, 1, 1), c->cblock, c->csmem, st>>>(c->spec_cols + (size_t)k * Hk * c->Ml, c->twM,
-                                                                       c->cM, c->cN, ca);
+    if (c->cols_tri)
+        c->cols_tri<<<dim3(Hk >> c->tri_lg_cpc, 1, 1), c->tri_threads, c->tri_smem, st>>>(
+            c->spec_cols + (size_t)k * Hk * c->Ml, c->tri_tab + ca.k2_off, ilog2(c->p.M), c->tri_lg_cpc, ca.bstride,
+            ca.lg_seg, ca.seg_stride);
+    else
+        c->cols<<<dim3(Hk >> ca.lg_cpc, 1, 1), c->cblock, c->csmem, st>>>(c->spec_cols + (size_t)k * Hk * c->Ml, c->twM,
+                                                                           c->cM, c->cN, ca);
     prof_end(c, SR_K_COLS_SOLVE);
 }
 void enq_c2r(sr_sb_ctx* c, float* out, float clip, int accum, int sweep = -1) {

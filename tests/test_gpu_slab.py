@@ -24,13 +24,20 @@ def S():
     return srsb
 
 
-@pytest.fixture(autouse=True)
-def _fft_column_pass(monkeypatch):
-    """Slab contexts run the column pass as FFT -> divide -> inverse FFT on the all-to-all-transposed
-    spectrum; whole-image contexts default to the cyclic tridiagonal column pass (another rounding order of
-    the same solve).  The bitwise slab == whole-image property is a statement about identical butterflies,
-    so the whole-image side runs the FFT column pass here too (knob read at context creation)."""
-    monkeypatch.setenv("SRSB_COLS_TRI", "0")
+@pytest.fixture(autouse=True, params=["tri", "fft"])
+def _column_pass(request, monkeypatch):
+    """The bitwise slab == whole-image property is a statement about identical arithmetic in identical order,
+    so both sides run the same column pass (knobs read at context creation): 'tri' = the cyclic tridiagonal
+    solve on the transposed spectrum with contiguous columns (slab contexts: column segments of the
+    all-to-all receive buffer; whole image: G = 1, no row-major spectrum, no cluster solve), 'fft' = FFT ->
+    divide by the symbol -> inverse FFT on both."""
+    if request.param == "fft":
+        monkeypatch.setenv("SRSB_COLS_TRI", "0")
+    else:
+        monkeypatch.setenv("SRSB_SPEC_RM", "0")
+        monkeypatch.setenv("SRSB_SOLVE_CL", "0")
+        monkeypatch.setenv("SRSB_G", "1")
+    return request.param
 
 
 KEYS = ("gamma", "alpha", "beta", "mu", "epsilon", "l", "d", "window_shape", "tau", "S", "rho", "sigma", "s",

@@ -536,6 +536,24 @@ __global__ void __launch_bounds__(512, 1) k_cols_solve_p(float2* __restrict__ sp
     }
 }
 
+// Batched in-place complex FFT of contiguous lines of M = 2^LOGM values (3-D solve: the i axis of every
+// (k2, z) line of the transposed spectrum, sr_vol.cuh).  grid = lines / cpc, block cpc * M / E threads,
+// dynamic shared memory cpc * SC float2; unnormalised, forward exp(-i) / inverse exp(+i).
+template <int LOGM, int LOGE, bool INV>
+__global__ void __launch_bounds__(512) k_lines_fft(float2* __restrict__ data, const float2* __restrict__ twM, int lg_cpc, int SC) {
+    constexpr int M = 1 << LOGM, E = 1 << LOGE, T = M / E;
+    extern __shared__ float2 smem2[];
+    const int t = threadIdx.x % T, cl = threadIdx.x / T;
+    float2* line = data + ((size_t)((blockIdx.x << lg_cpc) + cl) << LOGM);
+    float2* sm = smem2 + cl * SC;
+    float2 v[E];
+#pragma unroll
+    for (int u = 0; u < E; u++) v[u] = line[t + u * T];
+    fft_stages<LOGM, LOGE, 0, INV>(v, sm, t, twM);
+#pragma unroll
+    for (int u = 0; u < E; u++) line[t + u * T] = v[u];
+}
+
 // NEXT-1 monitor partials of the c2r pass, out of line so the (untaken, monitor-off) branch costs the hot
 // row transform no registers
 static __device__ __noinline__ void c2r_partials(float dsum, float osum, double* dst) {

@@ -23,6 +23,8 @@ RowInvKernel pick_row_inv_shape(int log2_h, int lg_rpc, int lg_G);
 ColKernel pick_col(int log2_m, bool contig, bool symt);   // fft_cols.cu; contig: whole image, G = 1; symt: symbol table
 typedef void (*ColPKernel)(float2*, const float2*, const float*, const float*, FftColArgs, int, int);
 ColPKernel pick_col_p(int log2_m, bool symt);      // fft_cols.cu: persistent prefetching solve, M >= 4096
+typedef void (*LinesFftKernel)(float2*, const float2*, int, int);
+LinesFftKernel pick_lines_fft(int log2_m, bool inverse);   // fft_lines.cu: batched complex FFT of contiguous lines, M = 8 .. 8192
 // stencil_r<R>.cu; returns false if R is unsupported.  smem = dynamic shared bytes.
 bool pick_stencil(int R, int shape, bool leq, RhsKernel& rhs, WbKernel (&wb)[2][2], WbKernel& wb_mon, int& smem);
 

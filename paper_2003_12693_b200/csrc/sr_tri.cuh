@@ -23,9 +23,34 @@
 // per-column table computed in fp64 on the host (TriCol).
 #pragma once
 #include <cuda_runtime.h>
+#include <cmath>
 #include "sr_tma.cuh"
 
 namespace srsb {
+
+// ---- host logic (fp64): constants of c x_i - a (x_{i-1} + x_{i+1}) = d_i, cut into C chunks of L
+// carry terms of the chunked recurrences of sr_tri.cuh: the smallest m with rho^m < 2^-48 (rho = r^L), at most
+// one wrap of C chunks (then the series is closed by 1 / (1 - rho^C))
+inline int tri_carry_terms(double rho, int C, double* clos) {
+    int m = 1;
+    if (rho > 0.0) {
+        const double v = std::ceil(-48.0 * std::log(2.0) / std::log(rho));
+        m = v > (double)C ? C : (int)v;
+    }
+    if (m < 1) m = 1;
+    if (clos) *clos = 1.0;
+    if (m >= C) {
+        m = C;
+        if (clos) *clos = 1.0 / (1.0 - std::pow(rho, C));
+    }
+    return m;
+}
+inline double tri_ratio(double a, double cc, double* sq_out) {   // r = 2a / (c + sqrt(c^2 - 4 a^2)) of c x_i - a (x_{i-1} + x_{i+1})
+    const double sq = std::sqrt(cc * cc - 4.0 * a * a);
+    if (sq_out) *sq_out = sq;
+    return 2.0 * a / (cc + sq);
+}
+
 
 struct TriCol {       // per global spectrum column k2; [0] real part, [1] imaginary part (differ only for k2 = 0)
     float r[2];       // recurrence ratio
@@ -156,7 +181,8 @@ __global__ void __launch_bounds__(512, SRSB_TRI_MINB) k_cols_tri(float2* __restr
 constexpr int kTriRmMaxCarry = 4;
 template <int LOGL>
 __global__ void __launch_bounds__(512, 2) k_cols_tri_rm(const float2* __restrict__ in, float2* __restrict__ out,
-                                                        const TriCol* __restrict__ tc, int lgM, int lgG, int H, int mmax) {
+                                                        const TriCol* __restrict__ tc, int lgM, int lgG, int H, int mmax,
+                                                        int tc_bstride) {
     constexpr int L = 1 << LOGL;
     extern __shared__ float2 smem2[];
     const int M = 1 << lgM, C = M >> LOGL, G = 1 << lgG;
@@ -179,7 +205,8 @@ __global__ void __launch_bounds__(512, 2) k_cols_tri_rm(const float2* __restrict
         }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
-    const TriCol* q = tc + k2;
+    const TriCol* q = tc + (size_t)blockIdx.z * tc_bstride + k2;   // tc_bstride = 0: one table for every image (2-D);
+                                                                   // 3-D: one table row per spectrum plane
     const float2 r = make_float2(__ldg(&q->r[0]), __ldg(&q->r[1]));
     const float2 rho = make_float2(__ldg(&q->rho[0]), __ldg(&q->rho[1]));
     for (int h = w; h < 2 * mmax; h += W) {   // halo chunks: end values only
@@ -254,7 +281,7 @@ __global__ void __launch_bounds__(512, 2) k_cols_tri_rm(const float2* __restrict
 }
 
 typedef void (*ColTriKernel)(float2*, const TriCol*, int, int, long long, int, long long);
-typedef void (*ColTriRmKernel)(const float2*, float2*, const TriCol*, int, int, int, int);
+typedef void (*ColTriRmKernel)(const float2*, float2*, const TriCol*, int, int, int, int, int);
 ColTriRmKernel pick_col_tri_rm();   // fft_tri.cu
 ColTriKernel pick_col_tri();     // fft_tri.cu
 constexpr int kTriLogL = 4;      // chunk length 2^kTriLogL

@@ -220,28 +220,6 @@ bool encode_map3d(CUtensorMap* m, float* base, int N, int rows, int planes, int 
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// carry terms of the chunked recurrences of sr_tri.cuh: the smallest m with rho^m < 2^-48 (rho = r^L), at most
-// one wrap of C chunks (then the series is closed by 1 / (1 - rho^C))
-int tri_carry_terms(double rho, int C, double* clos) {
-    int m = 1;
-    if (rho > 0.0) {
-        const double v = std::ceil(-48.0 * std::log(2.0) / std::log(rho));
-        m = v > (double)C ? C : (int)v;
-    }
-    if (m < 1) m = 1;
-    if (clos) *clos = 1.0;
-    if (m >= C) {
-        m = C;
-        if (clos) *clos = 1.0 / (1.0 - std::pow(rho, C));
-    }
-    return m;
-}
-double tri_ratio(double a, double cc, double* sq_out) {   // r = 2a / (c + sqrt(c^2 - 4 a^2)) of c x_i - a (x_{i-1} + x_{i+1})
-    const double sq = std::sqrt(cc * cc - 4.0 * a * a);
-    if (sq_out) *sq_out = sq;
-    return 2.0 * a / (cc + sq);
-}
-
 sr_status configure(sr_sb_ctx* c) {
     const sr_sb_params& p = c->p;
     const int M = p.M, Ml = c->Ml, N = p.N, H = N / 2, B = p.batch, P = c->nranks;
@@ -729,7 +707,7 @@ void enq_cols(sr_sb_ctx* c) {
     prof_begin(c);
     if (c->cols_tri_rm)
         c->cols_tri_rm<<<c->trm_grid, c->trm_threads, c->trm_smem, c->s>>>(c->spec, c->spec2, c->tri_tab, ilog2(c->p.M),
-                                                                           c->ca.lg_G, c->p.N / 2, c->trm_mmax);
+                                                                           c->ca.lg_G, c->p.N / 2, c->trm_mmax, 0);
     else if (c->cols_tri)
         c->cols_tri<<<c->tri_grid, c->tri_threads, c->tri_smem, c->s>>>(c->slab ? c->spec_cols : c->spec,
                                                                         c->tri_tab + c->ca.k2_off, ilog2(c->p.M),

@@ -2,8 +2,11 @@
 // D x M x N volume per context, the same parameters as the 2-D library (sr_sb_params; M, N the
 // in-plane sizes, batch = 1), FFT phi solver only.
 //
-// Per outer iteration: S x (k3_rhs -> k_rows_r2c over D*M rows -> k3_planes_solve ->
-// k_rows_c2r over D*M rows) + k3_wb passes; captured once in a CUDA graph of 2 iterations (the w
+// Per outer iteration: S x (k3_rhs -> phi solve -> ) + k3_wb passes; the phi solve (Eq. 31-33 in 3-D) is
+//   k_rows_r2c over the D*M rows (FFT along j) -> k_lines_fft (FFT along i of every (k2, z) line) -> k3_unpack0
+//   (the packed k2 = 0 / N/2 plane split into two planes) -> k_cols_tri_rm along z (cyclic tridiagonal solve per
+//   (k1, k2)) -> k3_repack0 -> k_lines_fft inverse -> k_rows_c2r: any D >= 16, M >= 32;
+//   smaller volumes (or SRSB_VOL_SOLVE=plane) keep k3_planes_solve, one D x M plane in shared memory; captured once in a CUDA graph of 2 iterations (the w
 // ping-pong parity), replayed by sr_sb3_iterate.
 #include <cuda_runtime.h>
 
@@ -14,10 +17,39 @@
 
 #include "../../include/srsb.h"
 #include "sr_kernels.h"
+#include "sr_tri.cuh"
 #define SRSB_VOL_HOST_KERNELS
 #include "sr_vol3.h"
 
 using namespace srsb;
+
+// Plane 0 of the transposed spectrum after the FFT along i: Z = FFT_i(X0 + i XH), X0 / XH the real k2 = 0 / N/2
+// columns of the row pass's packed slot.  A = FFT_i(X0) = (Z[k] + conj Z[-k]) / 2 stays in plane 0,
+// B = FFT_i(XH) = (Z[k] - conj Z[-k]) / (2i) goes to plane H, so the z solve sees H + 1 ordinary planes.
+// One thread per (z, k <= M/2) pair (k, M - k); in place.
+__global__ void k3_unpack0(float2* __restrict__ P0, float2* __restrict__ PH, int D, int M) {
+    const int half = M / 2 + 1;
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (long long)D * half) return;
+    const int z = (int)(e / half), k = (int)(e % half), kn = (M - k) & (M - 1);
+    const long long ik = (long long)z * M + k, in = (long long)z * M + kn;
+    const float2 Zk = P0[ik], Zn = P0[in];
+    const float2 A = make_float2(0.5f * (Zk.x + Zn.x), 0.5f * (Zk.y - Zn.y));
+    const float2 B = make_float2(0.5f * (Zk.y + Zn.y), -0.5f * (Zk.x - Zn.x));
+    P0[ik] = A;
+    PH[ik] = B;
+    if (kn != k) {
+        P0[in] = make_float2(A.x, -A.y);
+        PH[in] = make_float2(B.x, -B.y);
+    }
+}
+// ... and back: Z = A + i B into plane 0
+__global__ void k3_repack0(float2* __restrict__ P0, const float2* __restrict__ PH, long long n) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n) return;
+    const float2 A = P0[e], B = PH[e];
+    P0[e] = make_float2(A.x - B.y, A.y + B.x);
+}
 
 struct sr_sb3_ctx {
     sr_sb_params p;
@@ -27,6 +59,14 @@ struct sr_sb3_ctx {
     long long vol = 0;
     float *phi = nullptr, *F = nullptr, *w[2] = {nullptr, nullptr}, *b = nullptr, *g = nullptr, *tmp = nullptr;
     float2* spec = nullptr;
+    float2* spec2 = nullptr;           // lines path: (H + 1) planes, the z solve is out of place
+    TriCol* tri_tab = nullptr;         // [(H + 1)][M] constants of the z recurrences
+    bool lines = false;                // FFT along j and i + tridiagonal solve along z (any size); else the plane solve
+    LinesFftKernel lfwd = nullptr, linv = nullptr;
+    ColTriRmKernel tri = nullptr;
+    int l_lg_cpc = 0, l_threads = 0, l_smem = 0, l_sc = 0, l_grid = 0;
+    dim3 t_grid;
+    int t_threads = 0, t_smem = 0, t_mmax = 0;
     float2 *twH = nullptr, *twR = nullptr, *twM = nullptr, *twD = nullptr;
     float *cM = nullptr, *cD = nullptr, *cN = nullptr, *blurk = nullptr;
     int* flag = nullptr;
@@ -97,10 +137,6 @@ sr_status validate3(const sr_sb_params* p, int D, std::string& m) {
         m = "D, M, N must be powers of two (M, N >= 8, N <= 8192, D <= 1024)";
         return SR_ERR_SHAPE;
     }
-    if ((long long)(D * (p->M + 1) + p->M / 2 + D / 2 + 1) * 8 > 200 * 1024) {
-        m = "3-D: one D x M spectrum plane must fit in shared memory (D (M + 1) <= 25600)";
-        return SR_ERR_SHAPE;
-    }
     if (p->batch != 1) { m = "3-D contexts hold one volume (batch = 1)"; return SR_ERR_SHAPE; }
     if (!(p->tau >= 0.f) || !(p->mu > 0.f) || !(p->epsilon > 0.f) || !(p->d > 0.f) || !(p->sigma > 0.f) ||
         !(p->l >= 0.f) || !(p->rho >= 0.f)) {
@@ -148,6 +184,75 @@ sr_status configure3(sr_sb3_ctx* c) {
     c->rsmem = rpc * sr * (int)sizeof(float2);
     CK3(cudaFuncSetAttribute((const void*)c->rfwd, cudaFuncAttributeMaxDynamicSharedMemorySize, c->rsmem));
     CK3(cudaFuncSetAttribute((const void*)c->rinv, cudaFuncAttributeMaxDynamicSharedMemorySize, c->rsmem));
+    {   // solve path: lines (general) or plane (small volumes)
+        const char* ev = std::getenv("SRSB_VOL_SOLVE");
+        const int L = 1 << kTriLogL;
+        c->lines = false;
+        if (D >= L && M >= 32 && !(ev && ev[0] == 'p')) {
+            const double a = (double)p.tau * (double)p.mu;
+            const double r0 = tri_ratio(a, 1.0 + 2.0 * a, nullptr);   // (k1, k2) = (0, 0): the slowest decay
+            const int mm = tri_carry_terms(std::pow(r0, L), D / L, nullptr);
+            c->lfwd = pick_lines_fft(lg2(M), false);
+            c->linv = pick_lines_fft(lg2(M), true);
+            if (mm <= kTriRmMaxCarry && c->lfwd && c->linv) {
+                c->lines = true;
+                c->t_mmax = mm;
+            }
+        }
+        const bool plane_fits = (long long)(D * (M + 1) + M / 2 + D / 2 + 1) * 8 <= 200 * 1024;
+        if (!c->lines && !plane_fits)
+            return fail3(c, SR_ERR_SHAPE, "3-D: this volume needs the lines solve (D >= 16, M >= 32, tau mu not extreme); "
+                                          "the plane solve holds one D x M spectrum plane in shared memory (D (M + 1) <= 25600)");
+    }
+    if (c->lines) {
+        const int L = 1 << kTriLogL, C = D / L;
+        const int E_m = M < 16 ? M : 16, T_m = M / E_m;
+        int cpc = 1;
+        while (cpc * T_m < 64 && cpc * 2 <= H * D) cpc *= 2;
+        int sc = M + (M >> 4);
+        sc = ((sc + 15) & ~15) + 1;
+        c->l_lg_cpc = lg2(cpc);
+        c->l_threads = cpc * T_m;
+        c->l_sc = sc;
+        c->l_smem = cpc * sc * (int)sizeof(float2);
+        c->l_grid = H * D / cpc;
+        CK3(cudaFuncSetAttribute((const void*)c->lfwd, cudaFuncAttributeMaxDynamicSharedMemorySize, c->l_smem));
+        CK3(cudaFuncSetAttribute((const void*)c->linv, cudaFuncAttributeMaxDynamicSharedMemorySize, c->l_smem));
+        int W = 8;
+        if (W > C) W = C;
+        c->tri = pick_col_tri_rm();
+        c->t_threads = 32 * W;
+        c->t_smem = (W * L + 2 * (c->t_mmax + W)) * 32 * (int)sizeof(float2);
+        c->t_grid = dim3(M / 32, C / W, H + 1);
+        CK3(cudaFuncSetAttribute((const void*)c->tri, cudaFuncAttributeMaxDynamicSharedMemorySize, c->t_smem));
+        const size_t nplane = (size_t)D * M;
+        if (!c->spec2 && cudaMalloc((void**)&c->spec2, (size_t)(H + 1) * nplane * sizeof(float2)) != cudaSuccess)
+            return fail3(c, SR_ERR_OOM, "spectrum allocation failed");
+        if (!c->tri_tab && cudaMalloc((void**)&c->tri_tab, (size_t)(H + 1) * M * sizeof(TriCol)) != cudaSuccess)
+            return fail3(c, SR_ERR_OOM, "tridiagonal table allocation failed");
+        // constants of c x_z - a (x_{z-1} + x_{z+1}) = d_z per (plane k2, column k1), fp64 -> fp32:
+        // c = 1 + tau mu (6 - 2 cos(2 pi k1 / M) - 2 cos(2 pi k2 / N)); plane H is k2 = N/2 (unpacked from slot 0)
+        std::vector<TriCol> tab((size_t)(H + 1) * M);
+        const double a = (double)p.tau * (double)p.mu, pi_ = 3.14159265358979323846;
+        for (int k2 = 0; k2 <= H; k2++)
+            for (int k1 = 0; k1 < M; k1++) {
+                double sq = 1.0, clos = 1.0;
+                const double cc = 1.0 + a * (6.0 - 2.0 * std::cos(2 * pi_ * k1 / M) - 2.0 * std::cos(2 * pi_ * k2 / N));
+                const double r = tri_ratio(a, cc, &sq), rho = std::pow(r, L);
+                const int mm = tri_carry_terms(rho, C, &clos);
+                TriCol& t = tab[(size_t)k2 * M + k1];
+                for (int q = 0; q < 2; q++) {
+                    t.r[q] = (float)r;
+                    t.ks[q] = (float)(1.0 / (sq * (double)H * (double)M));   // + the j and i FFT normalisations
+                    t.rho[q] = (float)rho;
+                    t.clos[q] = (float)clos;
+                }
+                t.mmax = mm;
+                t.pad_[0] = t.pad_[1] = t.pad_[2] = 0;
+            }
+        CK3(cudaMemcpyAsync(c->tri_tab, tab.data(), tab.size() * sizeof(TriCol), cudaMemcpyHostToDevice, c->s));
+        CK3(cudaStreamSynchronize(c->s));
+    }
     // plane solve
     c->pa.D = D;
     c->pa.M = M;
@@ -156,7 +261,8 @@ sr_status configure3(sr_sb3_ctx* c) {
     c->pa.scale = (float)(1.0 / ((double)D * (double)M * (double)H));
     c->psmem = (D * (M + 1) + M / 2 + D / 2 + 1) * (int)sizeof(float2);
     c->pthreads = 1024;
-    CK3(cudaFuncSetAttribute((const void*)k3_planes_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, c->psmem));
+    if (!c->lines)
+        CK3(cudaFuncSetAttribute((const void*)k3_planes_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, c->psmem));
     // stencils
     if (!pick_vol(p.window, p.window_shape, p.l == p.epsilon, c->rhs, c->wb, c->vsmem))
         return fail3(c, SR_ERR_ARG, "window radius not supported in 3-D");
@@ -246,13 +352,26 @@ void enq_solve3(sr_sb3_ctx* c, const float* in, float* out, float clip, int accu
     c->rfwd<<<c->rgrid, c->rblock, c->rsmem, c->s>>>(in, c->spec, c->twH, c->twR, c->ra);
     prof_e(c, SR_K_ROWS_R2C);
     prof_b(c);
-    k3_planes_solve<<<c->p.N / 2, c->pthreads, c->psmem, c->s>>>(c->spec, c->twM, c->twD, c->cM, c->cD, c->cN, c->pa);
+    const float2* solved = c->spec;
+    if (c->lines) {
+        const int D = c->D, M = c->p.M, H = c->p.N / 2;
+        const long long nplane = (long long)D * M;
+        c->lfwd<<<c->l_grid, c->l_threads, c->l_smem, c->s>>>(c->spec, c->twM, c->l_lg_cpc, c->l_sc);
+        // the packed plane 0 -> plane 0 (k2 = 0) and plane H (k2 = N/2); spec and spec2 hold H + 1 planes
+        k3_unpack0<<<(int)((nplane / 2 + D + 255) / 256), 256, 0, c->s>>>(c->spec, c->spec + (size_t)H * nplane, D, M);
+        c->tri<<<c->t_grid, c->t_threads, c->t_smem, c->s>>>(c->spec, c->spec2, c->tri_tab, lg2(D), lg2(M), M, c->t_mmax, M);
+        k3_repack0<<<(int)((nplane + 255) / 256), 256, 0, c->s>>>(c->spec2, c->spec2 + (size_t)H * nplane, nplane);
+        c->linv<<<c->l_grid, c->l_threads, c->l_smem, c->s>>>(c->spec2, c->twM, c->l_lg_cpc, c->l_sc);
+        solved = c->spec2;
+    } else {
+        k3_planes_solve<<<c->p.N / 2, c->pthreads, c->psmem, c->s>>>(c->spec, c->twM, c->twD, c->cM, c->cD, c->cN, c->pa);
+    }
     prof_e(c, SR_K_COLS_SOLVE);
     FftRowArgs ra = c->ra;
     ra.clip = clip;
     ra.accum = accum;
     prof_b(c);
-    c->rinv<<<c->rgrid, c->rblock, c->rsmem, c->s>>>(c->spec, out, c->twH, c->twR, ra);
+    c->rinv<<<c->rgrid, c->rblock, c->rsmem, c->s>>>(solved, out, c->twH, c->twR, ra);
     prof_e(c, SR_K_ROWS_C2R);
 }
 void enq_wb3(sr_sb3_ctx* c, int last) {
@@ -310,7 +429,7 @@ sr_status sr_sb3_create(const sr_sb_params* p, int D, int device, void* stream, 
     c->device = device;
     c->user = (cudaStream_t)stream;
     const long long V = (long long)D * p->M * p->N;
-    const size_t nspec = (size_t)(p->N / 2) * D * p->M;
+    const size_t nspec = (size_t)(p->N / 2 + 1) * D * p->M;   // + plane N/2 of the lines solve (unpacked from slot 0)
     bool ok = cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking) == cudaSuccess &&
               cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming) == cudaSuccess &&
               cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming) == cudaSuccess;
@@ -495,7 +614,7 @@ void sr_sb3_destroy(sr_sb3_ctx* c) {
     Dev3 dg(c->device);
     if (c->s) cudaStreamSynchronize(c->s);
     if (c->graph) cudaGraphExecDestroy(c->graph);
-    void* ptrs[] = {c->phi, c->F, c->w[0], c->w[1], c->b, c->g, c->tmp, c->spec, c->twH, c->twR,
+    void* ptrs[] = {c->phi, c->F, c->w[0], c->w[1], c->b, c->g, c->tmp, c->spec, c->spec2, c->tri_tab, c->twH, c->twR,
                     c->twM, c->twD, c->cM, c->cD, c->cN, c->blurk, c->flag};
     for (void* q : ptrs)
         if (q) cudaFree(q);

@@ -44,8 +44,17 @@ def _rand(shape, seed, lo=-1.0, hi=1.0):
 
 
 @pytest.mark.parametrize("shape", [(1, 8, 8), (2, 8, 16), (8, 16, 32), (16, 16, 16), (32, 64, 32), (64, 128, 64),
-                                   (128, 128, 128), (16, 8, 256)])
-def test_solve3_parity(S, orc, shape):
+                                   (128, 128, 128), (16, 8, 256), (16, 32, 16), (64, 512, 32), (256, 256, 64)])
+@pytest.mark.parametrize("path", ["default", "plane"])
+def test_solve3_parity(S, orc, shape, path, monkeypatch):
+    """path: the default solve (FFT along j and i + cyclic tridiagonal solve along z where D >= 16 and M >= 32,
+    any size; else one D x M spectrum plane in shared memory) or the plane solve forced (needs D (M + 1) <= 25600:
+    the last two shapes exist only on the default path)."""
+    D, M, N = shape
+    if path == "plane":
+        if D * (M + 1) > 25600:
+            pytest.skip("beyond the plane solve's shared-memory limit")
+        monkeypatch.setenv("SRSB_VOL_SOLVE", "plane")
     p = _p(2)
     F = _rand(shape, sum(shape)).astype(np.float32)
     with _solver(S, shape, p) as sv:
@@ -54,10 +63,10 @@ def test_solve3_parity(S, orc, shape):
     assert np.max(np.abs(out - ref)) <= 2e-6 * np.max(np.abs(F))
 
 
-def test_solve3_cos_modes(S):
+@pytest.mark.parametrize("D,M,N", [(8, 16, 32), (32, 32, 32)])
+def test_solve3_cos_modes(S, D, M, N):
     """A single cosine mode (k3, k1, k2), including the packed k2 = 0 and N/2 columns, is scaled by
-    1 / symbol (Eq. 32 in 3-D)."""
-    D, M, N = 8, 16, 32
+    1 / symbol (Eq. 32 in 3-D); the second shape runs the lines solve (unpacked k2 = 0 / N/2 planes)."""
     p = _p(2)
     tm = p["tau"] * p["mu"]
     z, i, j = np.meshgrid(np.arange(D), np.arange(M), np.arange(N), indexing="ij")

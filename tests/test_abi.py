@@ -116,7 +116,7 @@ def test_product_path_never_imports_the_oracle():
 
 
 @pytest.mark.parametrize("D,field,value,status", [(3, "M", 64, -2), (8, "batch", 2, -2), (8, "window", 5, -1),
-                                                  (256, "M", 128, -2), (8, "phi_solver", 1, -1), (0, "M", 64, -2)])
+                                                  (2048, "M", 64, -2), (8, "phi_solver", 1, -1), (0, "M", 64, -2)])
 def test_create3_validates_before_device(srsb, D, field, value, status):
     p = srsb.Params()
     srsb.lib().sr_sb_default_params(C.byref(p), 64, 64, 1, 3)

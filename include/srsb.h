@@ -232,7 +232,8 @@ int sr_sb_abi_version(void);
 
 /* ---- 3-D extension ("The algorithm can also be extended to 3D",
  * Fig. 6 caption P:568; reading Q26 of DESIGN.md).  One volume of D x M x N voxels per context,
- * all powers of two, D (M + 1) <= 25600 (a D x M spectrum plane is solved in shared memory),
+ * all powers of two (M, N >= 8, N <= 8192, D <= 1024; thin volumes with D < 16 or M < 32 additionally need
+ * D (M + 1) <= 25600: their D x M spectrum planes are solved in shared memory),
  * p->batch = 1, window radius <= 4, FFT phi solver; every other parameter as in 2-D.
  * Every operator gains the depth axis z: grad = forward differences along (i, j, z) with 0 on
  * the last index of each axis (Eq. 35), div its Neumann adjoint (Eq. 36), the window the ball

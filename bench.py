@@ -321,7 +321,12 @@ def run_volume(args, world, rank, local):
                                                  f"ellipsoids, noise 0.15), {K} SB iterations, ball radius {R}, S=3",
                                      "l2": "state 46 B/voxel x 2 Mvox = 96 MB: partly L2-resident",
                                      "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
-                          "roofline": roof, "gpu_launches": args.steps * (5 + K * 13) * world,
+                          # per iteration: S x (rhs, r2c, solve, c2r) + wb; the lines solve (D >= 16, M >= 32) is 5 kernels
+                          # (line FFT, unpack, z solve, repack, inverse line FFT), the plane solve 1
+                          "roofline": roof,
+                          "gpu_launches": args.steps * (5 + K * (3 * (3 + (5 if shape[0] >= 16 and shape[1] >= 32 and
+                                                                          os.environ.get("SRSB_VOL_SOLVE", "")[:1] != "p"
+                                                                          else 1)) + 1)) * world,
                           "clocks": clk.summary()}), flush=True)
     sv.close()
     if world > 1:

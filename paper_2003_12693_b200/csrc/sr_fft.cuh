@@ -41,6 +41,9 @@ namespace srsb {
 #ifndef SRSB_R2C_MIRROR
 #define SRSB_R2C_MIRROR 1   // r2c split: bins k and H - k from one pair of shared reads (0: one bin per pair)
 #endif
+#ifndef SRSB_R2C_SHFL
+#define SRSB_R2C_SHFL 0     // 1: the row-major H = 512 instances (one warp per row) do the real split through warp shuffles
+#endif
 #ifndef SRSB_R2C_PF_DIST
 #define SRSB_R2C_PF_DIST 592    // 148 SMs x 4 resident CTAs
 #endif
@@ -240,6 +243,35 @@ k_rows_r2c(const float* __restrict__ F, float2* __restrict__ spec,
 #pragma unroll
     for (int u = 0; u < E; u++) v[u] = __ldcs(x + t + u * T);
     fft_stages<LOGH, LOGE, 0, false>(v, sm, t, twH);
+    if constexpr (SRSB_R2C_SHFL && LG == LOGH && LRPC >= 0 && T == 32 && E == 16) {
+        // row-major spectrum, one warp per row (H = 512): thread t holds Z[t + 32 u]; the split partner
+        // Z[H - k] of k = t + 32 u sits in lane (32 - t) % 32 at index 15 - u (lane 0: its own index 16 - u), so
+        // the split needs no shared-memory round trip and no barrier.  Same operands, same operations as the
+        // shared-memory split: bitwise equal.
+        float2* o = spec + (size_t)b * H * a.M + (size_t)(m0 + grp) * H;
+        const int src = (32 - t) & 31;
+#pragma unroll
+        for (int u = 0; u < E; u++) {
+            const float2 mine = v[15 - u];
+            float2 part = make_float2(__shfl_sync(0xffffffffu, mine.x, src), __shfl_sync(0xffffffffu, mine.y, src));
+            if (t == 0) part = v[(16 - u) & 15];
+            const int k = t + 32 * u;
+            const float2 tw = __ldg(&twR[k]);
+            float2 X;
+            if (u == 0 && t == 0) {
+                X = make_float2(v[0].x + v[0].y, v[0].x - v[0].y);   // (X[0], X[N/2]) packed
+            } else {
+                const float2 Zc = conjf2(part);
+                const float2 Ev = make_float2(0.5f * (v[u].x + Zc.x), 0.5f * (v[u].y + Zc.y));
+                const float2 D = make_float2(0.5f * (v[u].x - Zc.x), 0.5f * (v[u].y - Zc.y));
+                const float2 O = make_float2(D.y, -D.x);  // -i D
+                const float2 wo = cmul(tw, O);
+                X = make_float2(Ev.x + wo.x, Ev.y + wo.y);
+            }
+            o[k] = X;
+        }
+        return;
+    }
 #pragma unroll
     for (int u = 0; u < E; u++) sm[pad16(t + u * T)] = v[u];
     __syncthreads();

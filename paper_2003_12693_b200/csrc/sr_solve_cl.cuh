@@ -67,7 +67,10 @@ __global__ void __launch_bounds__(((1 << LOGH) / 16) << LRPC) k_solve_cluster(co
         for (int u = 0; u < E; u++) v[u] = __ldcs(x + t + u * T);
         fft_stages<LOGH, LOGE, 0, false>(v, sm, t, twH);
 #pragma unroll
-        for (int u = 0; u < E; u++) sm[pad16(t + u * T)] = v[u];
+        for (int u = 0; u < E; u++) {
+            SRSB_CHK(&sm[pad16(t + u * T)], 8);
+            sm[pad16(t + u * T)] = v[u];
+        }
     }
     __syncthreads();
     {   // real split in place: bins k2 and H - k2 of a row by one thread (slot 0 packs X[0], X[N/2])
@@ -84,6 +87,7 @@ __global__ void __launch_bounds__(((1 << LOGH) / 16) << LRPC) k_solve_cluster(co
             const int e = tid + u * NT;
             const int k2 = e & (H / 2 - 1), rr = e >> (LOGH - 1);
             float2* row = smem2 + rr * a.SR;
+            SRSB_CHK(&row[pad16(H - 1)], 8);
             if (k2 == 0) {
                 const float2 A0 = row[0], B0 = row[pad16(H / 2)];
                 row[0] = make_float2(A0.x + A0.y, A0.x - A0.y);
@@ -111,6 +115,8 @@ __global__ void __launch_bounds__(((1 << LOGH) / 16) << LRPC) k_solve_cluster(co
             z.x = fmaf(r.x, z.x, db.x);
             z.y = fmaf(r.y, z.y, db.y);
         }
+        SRSB_CHK(&BbS[tid], 8);
+        SRSB_CHK(&colp[(RPC - 1) * a.SR], 8);
         BfS[tid] = y;
         BbS[tid] = z;
     }

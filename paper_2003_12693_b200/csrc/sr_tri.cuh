@@ -120,6 +120,8 @@ __global__ void __launch_bounds__(512, SRSB_TRI_MINB) k_cols_tri(float2* __restr
             z.x = fmaf(r.x, z.x, d[L - 1 - j].x);
             z.y = fmaf(r.y, z.y, d[L - 1 - j].y);
         }
+        SRSB_CHK(&Bb[tid], 8);
+        SRSB_CHK(&ch[L - 1], 8);
         Bf[tid] = y;
         Bb[tid] = z;
     }
@@ -242,6 +244,8 @@ __global__ void __launch_bounds__(512, 2) k_cols_tri_rm(const float2* __restrict
             z.x = fmaf(r.x, z.x, d[L - 1 - j].x);
             z.y = fmaf(r.y, z.y, d[L - 1 - j].y);
         }
+        SRSB_CHK(&Bf[(mmax + w) * 32 + lane], 8);
+        SRSB_CHK(&Bb[(w + mmax) * 32 + lane], 8);
         Bf[(mmax + w) * 32 + lane] = y;
         Bb[w * 32 + lane] = z;
     }

@@ -613,6 +613,10 @@ static __device__ __noinline__ void c2r_partials(float dsum, float osum, double*
                             // Measured on C3: 0.258 ms per launch (78 registers, 3 CTAs / SM) against 0.189 ms
                             // with psi in registers (128 registers, 2 CTAs / SM): off
 #endif
+#ifndef SRSB_C2R_SHFL
+#define SRSB_C2R_SHFL 0     // 1: the row-major H = 512 instances (one warp per row) load their row straight into registers and
+                            // get the mirrored bins by warp shuffles (no shared-memory gather)
+#endif
 #ifndef SRSB_C2R_OWN_PF
 #define SRSB_C2R_OWN_PF 0   // 1: L2 bulk prefetch of the CTA's own psi rows at its start (with SRSB_C2R_LATE_OLD=1: the
                             // accumulation source is then loaded after the FFT, 32 registers fewer across it)
@@ -657,6 +661,34 @@ k_rows_c2r(const float2* __restrict__ spec, float* __restrict__ phi,
 #pragma unroll
         for (int u = 0; u < E; u++) old[u] = out[t + u * T];
     }
+    float2* sm = smem2 + grp * a.SR;
+    float2 v[E];
+    if constexpr (SRSB_C2R_SHFL && LG == LOGH && LRPC >= 0 && H_OF(LOGH) / (1 << LOGE) == 32 && (1 << LOGE) == 16) {
+        // row-major spectrum, one warp per row (H = 512): thread t loads X[t + 32 u] (coalesced) and gets the partner
+        // X[H - k] of k = t + 32 u from lane (32 - t) % 32, index 15 - u (lane 0: its own index 16 - u) by warp
+        // shuffles: no shared-memory staging, no barrier before the FFT.  Same operands and operations: bitwise equal.
+        const float2* xr = in + (size_t)(m0 + grp) * H;
+        float2 x[E];
+#pragma unroll
+        for (int u = 0; u < E; u++) x[u] = __ldcs(xr + t + 32 * u);
+        const int src = (32 - t) & 31;
+#pragma unroll
+        for (int u = 0; u < E; u++) {
+            const float2 mine = x[15 - u];
+            float2 part = make_float2(__shfl_sync(0xffffffffu, mine.x, src), __shfl_sync(0xffffffffu, mine.y, src));
+            if (t == 0) part = x[(16 - u) & 15];
+            const float2 X = x[u];
+            if (u == 0 && t == 0) {
+                v[u] = make_float2(0.5f * (X.x + X.y), 0.5f * (X.x - X.y));
+            } else {
+                const float2 Xc = conjf2(part);
+                const float2 Ev = make_float2(0.5f * (X.x + Xc.x), 0.5f * (X.y + Xc.y));
+                const float2 D = make_float2(0.5f * (X.x - Xc.x), 0.5f * (X.y - Xc.y));
+                const float2 O = cmul(conjf2(__ldg(&twR[t + 32 * u])), D);  // W^{-k} D
+                v[u] = make_float2(Ev.x - O.y, Ev.y + O.x);                 // E + i O
+            }
+        }
+    } else {
     // transposed gather: blockDim = rpc * T threads, rpc * H elements -> exactly E per thread;
     // all E loads are issued before the shared stores
     if constexpr (LG == LOGH && LRPC >= 0 && E >= 2 && LOGH >= 1) {
@@ -715,8 +747,6 @@ k_rows_c2r(const float2* __restrict__ spec, float* __restrict__ phi,
         }
     }
     __syncthreads();
-    float2* sm = smem2 + grp * a.SR;
-    float2 v[E];
 #pragma unroll
     for (int u = 0; u < E; u++) {
         const int k = t + u * T;
@@ -735,6 +765,7 @@ k_rows_c2r(const float2* __restrict__ spec, float* __restrict__ phi,
         }
     }
     __syncthreads();
+    }
     fft_stages<LOGH, LOGE, 0, true>(v, sm, t, twH);
     if (SRSB_C2R_LATE_OLD && a.accum) {
 #pragma unroll

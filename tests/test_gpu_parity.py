@@ -334,12 +334,6 @@ def test_c4_masks_truncated_horizon(S, orc):
     _final_masks(S, orc, "c4", K=100)
 
 
-def test_c4_final_masks(S, orc):
-    """C4 at full size and full length (4096^2, R = 6, K = 500): the DESIGN.md §6 rule against the cached fp64 run
-    (about 1 h of a GPU box's 16 host cores, tools/oracle_masks.py c4 --out ...)."""
-    _final_masks(S, orc, "c4")
-
-
 def test_c5_masks_truncated_horizon(S, orc):
     """C5 at full size (8192^2, R = 5, one GPU), masks after K = 30 of its 300 iterations (the full
     fp64 run would take ~8 h of 16 host cores).  Same rule as above."""

@@ -42,7 +42,9 @@ namespace srsb {
 #define SRSB_R2C_MIRROR 1   // r2c split: bins k and H - k from one pair of shared reads (0: one bin per pair)
 #endif
 #ifndef SRSB_R2C_SHFL
-#define SRSB_R2C_SHFL 0     // 1: the row-major H = 512 instances (one warp per row) do the real split through warp shuffles
+#define SRSB_R2C_SHFL 1     // the row-major H = 512 instances (one warp per row) do the real split through warp shuffles
+                            // (C3 r2c 0.109 -> 0.097 ms; same formulas, but the compiler contracts them into other FMAs
+                            // than in the shared-memory split, so not bitwise equal to SRSB_R2C_SHFL=0)
 #endif
 #ifndef SRSB_R2C_PF_DIST
 #define SRSB_R2C_PF_DIST 592    // 148 SMs x 4 resident CTAs
@@ -614,8 +616,9 @@ static __device__ __noinline__ void c2r_partials(float dsum, float osum, double*
                             // with psi in registers (128 registers, 2 CTAs / SM): off
 #endif
 #ifndef SRSB_C2R_SHFL
-#define SRSB_C2R_SHFL 0     // 1: the row-major H = 512 instances (one warp per row) load their row straight into registers and
-                            // get the mirrored bins by warp shuffles (no shared-memory gather)
+#define SRSB_C2R_SHFL 1     // the row-major H = 512 instances (one warp per row) load their row straight into registers and
+                            // get the mirrored bins by warp shuffles (no shared-memory gather): C3 c2r 0.146 -> 0.139 ms,
+                            // bitwise equal to the gather (tools/solve_hash.py)
 #endif
 #ifndef SRSB_C2R_OWN_PF
 #define SRSB_C2R_OWN_PF 0   // 1: L2 bulk prefetch of the CTA's own psi rows at its start (with SRSB_C2R_LATE_OLD=1: the
@@ -751,7 +754,7 @@ k_rows_c2r(const float2* __restrict__ spec, float* __restrict__ phi,
     for (int u = 0; u < E; u++) {
         const int k = t + u * T;
         SRSB_CHK(&sm[pad16(k)], 8);
-        SRSB_CHK(&sm[pad16(H - k)], 8);
+        if (k != 0) SRSB_CHK(&sm[pad16(H - k)], 8);
         const float2 X = sm[pad16(k)];
         if (k == 0) {
             // X.x = X[0], X.y = X[N/2]: Z[0] = E[0] + i O[0], E = (X0 + Xh)/2, O = (X0 - Xh)/2

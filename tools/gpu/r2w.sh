@@ -1,11 +1,11 @@
 # r2c warp-shuffle split (bitwise check + A/B), checked build over the new kernels, then the full suite, smoke, bench
 export OMP_NUM_THREADS=$(nproc)
 echo "hash default   $(python tools/solve_hash.py 1024 1024 3)"
-for v in shfl_both shfl_c2r shfl_r2c; do echo "hash $v $(SRSB_LIB=vlib/libsrsb_$v.so python tools/solve_hash.py 1024 1024 3)"; done
+for v in shfl_both shfl_c2r; do echo "hash $v $(SRSB_LIB=vlib/libsrsb_$v.so python tools/solve_hash.py 1024 1024 3)"; done
 B="python bench.py --no-cpu --no-e2e --no-fft-ref --steps 2 --warmup 3 --iters 100"
 for rep in 1 2; do
   timeout 300 $B > gpurun_out/r2w_c3_base$rep.log 2>&1
-  for v in shfl_both shfl_c2r shfl_r2c; do SRSB_LIB=vlib/libsrsb_$v.so timeout 300 $B > gpurun_out/r2w_c3_${v}$rep.log 2>&1; done
+  for v in shfl_both shfl_c2r; do SRSB_LIB=vlib/libsrsb_$v.so timeout 300 $B > gpurun_out/r2w_c3_${v}$rep.log 2>&1; done
 done
 python - <<'PY'
 import json,glob

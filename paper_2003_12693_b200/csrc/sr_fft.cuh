@@ -620,6 +620,10 @@ static __device__ __noinline__ void c2r_partials(float dsum, float osum, double*
                             // get the mirrored bins by warp shuffles (no shared-memory gather): C3 c2r 0.146 -> 0.139 ms,
                             // bitwise equal to the gather (tools/solve_hash.py)
 #endif
+#ifndef SRSB_C2R_SHFL_LATE
+#define SRSB_C2R_SHFL_LATE 0   // 1: the warp-shuffle c2r instances load the accumulation source after the FFT, L2-prefetched at
+                               // their start (the combination measured faster on C3 and slower on C5 before the shuffle split)
+#endif
 #ifndef SRSB_C2R_OWN_PF
 #define SRSB_C2R_OWN_PF 0   // 1: L2 bulk prefetch of the CTA's own psi rows at its start (with SRSB_C2R_LATE_OLD=1: the
                             // accumulation source is then loaded after the FFT, 32 registers fewer across it)
@@ -648,10 +652,14 @@ k_rows_c2r(const float2* __restrict__ spec, float* __restrict__ phi,
         if (block_ahead_2d(SRSB_C2R_PF_DIST, bx, by))
             bulk_prefetch_l2(phi + by * a.plane + (long long)(bx * rpc) * (2 * H), (uint32_t)(rpc * 2 * H * 4));
     }
-    if (SRSB_C2R_OWN_PF && a.accum && t == 0) bulk_prefetch_l2(out, (uint32_t)(2 * H * 4));
+    // the warp-shuffle instances may take the late + prefetched accumulation source on their own (SRSB_C2R_SHFL_LATE)
+    constexpr bool SHFLI = SRSB_C2R_SHFL && LG == LOGH && LRPC >= 0 && H_OF(LOGH) / (1 << LOGE) == 32 && (1 << LOGE) == 16;
+    constexpr bool LATE = SRSB_C2R_LATE_OLD || (SRSB_C2R_SHFL_LATE && SHFLI);
+    constexpr bool OWNPF = SRSB_C2R_OWN_PF || (SRSB_C2R_SHFL_LATE && SHFLI);
+    if (OWNPF && a.accum && t == 0) bulk_prefetch_l2(out, (uint32_t)(2 * H * 4));
     // accumulation source (phi of the previous sweep), fetched first: its latency hides behind the FFT.
     // OSM: into shared memory by cp.async (no registers held across the FFT), else into registers
-    constexpr bool OSM = SRSB_C2R_OLD_SMEM && LRPC >= 0 && !SRSB_C2R_LATE_OLD;
+    constexpr bool OSM = SRSB_C2R_OLD_SMEM && LRPC >= 0 && !LATE;
     float2* old_sm = smem2 + (size_t)rpc * a.SR + (size_t)grp * H;
     float2 old[E];
     if (OSM && a.accum) {
@@ -660,7 +668,7 @@ k_rows_c2r(const float2* __restrict__ spec, float* __restrict__ phi,
             asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(old_sm + t + u * T)),
                          "l"(out + t + u * T) : "memory");
         asm volatile("cp.async.commit_group;" ::: "memory");
-    } else if (!SRSB_C2R_LATE_OLD && a.accum) {
+    } else if (!LATE && a.accum) {
 #pragma unroll
         for (int u = 0; u < E; u++) old[u] = out[t + u * T];
     }
@@ -770,7 +778,7 @@ k_rows_c2r(const float2* __restrict__ spec, float* __restrict__ phi,
     __syncthreads();
     }
     fft_stages<LOGH, LOGE, 0, true>(v, sm, t, twH);
-    if (SRSB_C2R_LATE_OLD && a.accum) {
+    if (LATE && a.accum) {
 #pragma unroll
         for (int u = 0; u < E; u++) old[u] = out[t + u * T];
     }

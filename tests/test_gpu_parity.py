@@ -327,11 +327,16 @@ def test_c3_final_masks(S, orc, image):
     _final_masks(S, orc, "c3", images=[image])
 
 
-def test_c4_masks_truncated_horizon(S, orc):
-    """C4 at full size (4096^2, R = 6), masks after K = 100 of its 500 iterations: the full-length fp64
-    run costs ~6 h of 8 host cores, the K = 100 one ~1 h.  Same rule, no ensemble:
-    agreement >= 0.999 and an identical component count."""
-    _final_masks(S, orc, "c4", K=100)
+@pytest.mark.parametrize("K", [100, pytest.param(400, marks=pytest.mark.xfail(
+    strict=False, reason="pre-registered rule not met on the component count: measured agreement 1.00000 (fewer than 1 pixel in "
+                         "10^5 differs) but 82 components against the oracle's 83 -- one few-pixel component; no fp64 "
+                         "ensemble exists at this horizon (53 min of a box's host cores per member), so the count is held "
+                         "to identical (DESIGN.md §6); reported, the bar is not moved"))])
+def test_c4_masks_truncated_horizon(S, orc, K):
+    """C4 at full size (4096^2, R = 6), masks after K = 100 and K = 400 of its 500 iterations: the full-length fp64
+    run takes ~64 min of a GPU box's 16 host cores, more than one 3600 s box call; K = 400 takes 51.
+    Same rule, no ensemble: agreement >= 0.999 and an identical component count."""
+    _final_masks(S, orc, "c4", K=K)
 
 
 @pytest.mark.parametrize("K", [30, 100])
